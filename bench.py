@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""Headline benchmark: Shouji pairs filtered per second at m=100, E=5 on N B200s.
+
+One JSON line on rank 0 (contract in the task statement; fields explained in
+DESIGN.md "Measurement"):
+
+* value  — device-resident throughput: K back-to-back launches of the fused
+  sm_100a kernel over this rank's 30M-pair shard (BASELINE.json configs[1] at
+  E=5: 50% planted pairs with k ~ U{0..10} edits, 50% independent pairs; ASCII
+  records generated on the device), timed with CUDA events on the launching
+  stream, max over ranks, summed over ranks (weak scaling: every rank owns its
+  own 30M pairs; no collective touches the data path).
+* e2e    — the same workload through the public host API
+  (pf_shouji_filter_batch) from pinned host records: H2D of every record,
+  kernel, D2H of the accept bitmap, every step (wall clock, max over ranks).
+* roofline — the fused kernel's algorithmic bytes (2m ASCII + 1/8 accept bit per
+  pair) over its average launch time, against MEASURED_PEAKS.json hbm_gbs; the
+  INT view (BASELINE.md formula and the measured LOP3 lane rate) is reported
+  beside it.
+* cpu_baseline — the unmodified reference library (oracle/_ref) on this host's
+  cores over a bounded sample of the same records (rank 0, N=1 only).
+
+``--impl reference`` runs only the reference CPU path (rank 0) and prints its line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Shouji pairs filtered/sec (m=100,E=5)"
+UNIT = "pairs/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--pairs", type=int, default=30_000_000, help="pairs per GPU")
+    ap.add_argument("--m", type=int, default=100)
+    ap.add_argument("--e", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=4.0, help="target seconds per CPU pass")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def lscpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+        self.marks = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.perf_counter(), line.strip()))
+
+    def mark(self, name):
+        self.marks.append((name, time.perf_counter()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = []
+        for ts, line in self.samples:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            rows.append((ts, parts))
+        window = [p for ts, p in rows if t0 - 0.05 <= ts <= t1 + 0.05] or [p for _, p in rows]
+        if not window:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(p[1]) for p in window if p[1].replace(".", "").isdigit()]
+        mx = [float(p[2]) for p in window if p[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in window for i in range(4) if p[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(window),
+                "power_w_max": max((float(p[3]) for p in window
+                                    if p[3].replace(".", "").isdigit()), default=None)}
+
+
+# ------------------------------------------------------------------------------------
+# CPU baseline: the unmodified reference library on this host's cores
+# ------------------------------------------------------------------------------------
+def cpu_baseline(text, pattern, e, target_s, threads=None):
+    from oracle.oracle import Oracle, Reference
+    kind = "reference" if Reference.available() else "port"
+    lib = Reference() if kind == "reference" else Oracle()
+    threads = threads or (lib.hardware_concurrency() if kind == "reference" else os.cpu_count())
+    n_all = text.shape[0]
+    # size the sample so one timed pass takes ~target_s
+    probe = min(n_all, 20_000)
+    t0 = time.perf_counter()
+    lib.shouji_batch(text[:probe], pattern[:probe], e, threads=threads, estimates=False)
+    rate = probe / max(time.perf_counter() - t0, 1e-6)
+    n = int(min(n_all, max(probe, rate * target_s)))
+    t, p = text[:n], pattern[:n]
+    times = []
+    if kind == "reference":
+        packed = lib.pack(t, p)  # packing excluded from timing, as run_bench does (bench.cpp:24-25)
+        try:
+            packed.shouji(e, threads=threads, estimates=False)  # warm-up pass (bench.cpp:20-32)
+            for _ in range(3):
+                t0 = time.perf_counter()
+                packed.shouji(e, threads=threads, estimates=False)
+                times.append(time.perf_counter() - t0)
+        finally:
+            packed.free()
+    else:
+        lib.shouji_batch(t, p, e, threads=threads, estimates=False)
+        for _ in range(3):
+            t0 = time.perf_counter()
+            lib.shouji_batch(t, p, e, threads=threads, estimates=False)
+            times.append(time.perf_counter() - t0)
+    med = float(np.median(times))
+    return {"value": n / med, "unit": UNIT, "cores": int(threads), "kind": kind,
+            "sample": f"first {n} pairs of this run's workload (m={text.shape[1]}, E={e}), "
+                      f"pre-packed, median of 3 passes after 1 warm-up, {threads} threads "
+                      f"(parallel_for_pairs), CPU: {lscpu_model()}"}
+
+
+def reference_workload(n, m, e, seed):
+    """CPU-generated sample of BASELINE configs[1] at E: even pairs planted by the
+    reference generator (k ~ U{0..2E}, dataset.cpp:71-126), odd pairs independent."""
+    from oracle.oracle import Oracle, Reference
+    gen = Reference() if Reference.available() else Oracle()
+    half = (n + 1) // 2
+    t_pl, p_pl = gen.generate_pairs(seed, half, m, 0, min(2 * e, m))
+    rng = np.random.default_rng(seed)
+    alpha = np.frombuffer(b"ACGT", np.uint8)
+    t = np.empty((n, m), np.uint8)
+    p = np.empty((n, m), np.uint8)
+    t[0::2], p[0::2] = t_pl[: (n + 1) // 2], p_pl[: (n + 1) // 2]
+    t[1::2] = alpha[rng.integers(0, 4, size=(n // 2, m))]
+    p[1::2] = alpha[rng.integers(0, 4, size=(n // 2, m))]
+    return t, p
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from oracle.oracle import Oracle, Reference
+    kind = "reference" if Reference.available() else "port"
+    lib = Reference() if kind == "reference" else Oracle()
+    threads = lib.hardware_concurrency() if kind == "reference" else (os.cpu_count() or 1)
+    # bounded sample per step: ~2.5 s of CPU work per step
+    t, p = reference_workload(40_000, args.m, args.e, 1809078581 + 1000 * args.e)
+    t0 = time.perf_counter()
+    lib.shouji_batch(t, p, args.e, threads=threads, estimates=False)
+    rate = t.shape[0] / max(time.perf_counter() - t0, 1e-6)
+    n = int(min(4_000_000, max(40_000, rate * 2.5)))
+    t, p = reference_workload(n, args.m, args.e, 1809078581 + 1000 * args.e)
+    packed = lib.pack(t, p) if kind == "reference" else None
+    run = (lambda: packed.shouji(args.e, threads=threads, estimates=False)) if packed else \
+        (lambda: lib.shouji_batch(t, p, args.e, threads=threads, estimates=False))
+    for _ in range(args.warmup):
+        run()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    if packed:
+        packed.free()
+    total = sum(times)
+    value = n * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (CPU-generated sample of BASELINE configs[1] at E=5)",
+        "config": {"workload": f"configs[1] m={args.m} E={args.e}: bounded sample of {n} pairs "
+                               f"per step on the host CPU", "m": args.m, "E": args.e,
+                   "pairs_per_step": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(threads), "kind": kind,
+                         "sample": f"{n} pairs per step (50% planted k~U{{0..{2 * args.e}}} by the "
+                                   f"reference generator, 50% independent), pre-packed, "
+                                   f"parallel_for_pairs with {threads} threads, CPU: {lscpu_model()}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1809_07858_b200 as pf
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ctx = pf.Context([local_rank])
+    n, m, e = args.pairs, args.m, args.e
+    pitch = pf.device_pitch(m)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+
+    # ---- workload: configs[1] at E on this rank's device ---------------------------
+    text = torch.empty((n, pitch), dtype=torch.uint8, device=dev)
+    pattern = torch.empty((n, pitch), dtype=torch.uint8, device=dev)
+    seed = 1809078581 + 1000 * e + 7919 * rank
+    pf.generate_device(1, seed, e, text.data_ptr(), pattern.data_ptr(), pitch, n, m, stream=sh,
+                       ctx=ctx)
+    accept = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev)
+    errflag = torch.zeros(1, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize(dev)
+
+    def step():
+        pf.shouji_filter_device_async(text.data_ptr(), pattern.data_ptr(), pitch, n, m, e,
+                                      accept.data_ptr(), errflag.data_ptr(), stream=sh, ctx=ctx)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    gpu_index = local_rank
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        try:
+            gpu_index = int(vis.split(",")[local_rank])
+        except Exception:
+            pass
+    clocks = ClockSampler(gpu_index)
+    clocks.start()
+    time.sleep(0.3)
+
+    # ---- timed: K launches, events on the launching stream ---------------------------
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = pf.launch_count()
+    t_wall0 = time.perf_counter()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    end.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t_wall1 = time.perf_counter()
+    launches = pf.launch_count() - launches0
+    elapsed_ms = start.elapsed_time(end)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    time.sleep(0.1)
+
+    assert int(errflag.item()) == 0, "illegal bytes in the generated workload"
+    # spot-check the timed kernel's output against the CPU oracle (outside the timed region)
+    from oracle.oracle import Oracle
+    chk = 8192
+    t_h = text[:chk, :m].cpu().numpy()
+    p_h = pattern[:chk, :m].cpu().numpy()
+    a_ref, _, _ = Oracle().shouji_batch(t_h, p_h, e, estimates=False)
+    a_gpu = accept[: chk // 32].cpu().numpy().view(np.uint32)
+    assert (a_gpu == a_ref).all(), "benchmarked kernel disagrees with the oracle"
+
+    # ---- e2e: public host API from pinned host records ----------------------------------
+    e2e = None
+    t_e2e = (t_wall1, t_wall1)
+    if not args.no_e2e:
+        h_text = torch.empty((n, m), dtype=torch.uint8, pin_memory=True)
+        h_pattern = torch.empty((n, m), dtype=torch.uint8, pin_memory=True)
+        h_text.copy_(text[:, :m])
+        h_pattern.copy_(pattern[:, :m])
+        tn, pn = h_text.numpy(), h_pattern.numpy()
+        # free the device-resident copy so the host path owns device memory
+        del text, pattern
+        torch.cuda.empty_cache()
+        for _ in range(1):
+            pf.shouji_filter_batch(tn, pn, e, ctx=ctx)
+        if world > 1:
+            dist.barrier()
+        tw = []
+        t_e2e0 = time.perf_counter()
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            acc_h, _, _ = pf.shouji_filter_batch(tn, pn, e, ctx=ctx)  # H2D + kernel + D2H + sync
+            tw.append(time.perf_counter() - t0)
+        t_e2e = (t_e2e0, time.perf_counter())
+        assert (acc_h[: chk // 32] == a_ref).all()
+        e2e_s = sum(tw) / len(tw)
+        if world > 1:
+            tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        e2e = {"value": world * n / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(2 * n * m), "d2h_bytes_per_step": int(4 * ((n + 31) // 32)),
+               "ms_per_step": 1e3 * e2e_s,
+               "path": "pf_shouji_filter_batch(pinned host records, stride=m) -> H2D, fused kernel, "
+                       "D2H accept bitmap, sync"}
+    clocks.stop()
+
+    # ---- max over ranks ---------------------------------------------------------------
+    step_ms = elapsed_ms / args.steps
+    kern_avg_ms = float(np.mean(kern_ms))
+    if world > 1:
+        tt = torch.tensor([step_ms, kern_avg_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms, kern_avg_ms = float(tt[0]), float(tt[1])
+    value = world * n / (step_ms * 1e-3)
+
+    # ---- roofline -----------------------------------------------------------------------
+    peaks, peak_src = measured_peaks()
+    alg_bytes = n * (2 * m + 1 / 8)  # ASCII text+pattern in, one accept bit out
+    achieved_gbs = alg_bytes / (kern_avg_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("pairs") and tj.get("dram_bytes_per_launch"):
+                traffic = float(tj["dram_bytes_per_launch"]) * n / float(tj["pairs"])
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": float(peaks["hbm_gbs"]),
+                "unit": "GB/s", "frac": achieved_gbs / float(peaks["hbm_gbs"]), "traffic": traffic,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                "algorithmic_bytes_per_pair": 2 * m + 1 / 8,
+                "kernel": "sb::shouji_fused_w4<5> (fused pack+map+search+commit+accept)",
+                "kernel_ms_avg": kern_avg_ms}
+    int_view = None
+    if rank == 0:
+        try:
+            lop3 = pf.int_peak("lop3", ctx=ctx)
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            ops_pair = 25 * (2 * e + 1) * ((m + 31) // 32) + 8 * m  # BASELINE.md OPS(m,E)
+            int_bound = lop3 / ops_pair
+            int_view = {"ops_per_pair_formula": ops_pair, "lop3_lane_ops_per_s": lop3,
+                        "lop3_lanes_per_clk_per_sm_at_max_clock":
+                            lop3 / (sms * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6),
+                        "int_bound_pairs_per_s_per_gpu": int_bound,
+                        "frac_of_int_bound": (value / world) / int_bound,
+                        "hbm_bound_pairs_per_s_per_gpu":
+                            float(peaks["hbm_gbs"]) * 1e9 / (2 * m + 1 / 8)}
+        except Exception as ex:  # diagnostic only
+            int_view = {"error": str(ex)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        nb = 4_000_000
+        tb = np.empty((nb, m), np.uint8)
+        pb = np.empty((nb, m), np.uint8)
+        if e2e is not None:
+            tb[:] = tn[:nb]
+            pb[:] = pn[:nb]
+        else:
+            tb[:] = text[:nb, :m].cpu().numpy()
+            pb[:] = pattern[:nb, :m].cpu().numpy()
+        cpu = cpu_baseline(tb, pb, e, args.cpu_seconds)
+
+    ck = clocks.summary(t_wall0, t_wall1)
+    ck_e2e = clocks.summary(*t_e2e) if e2e is not None else None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (device-generated BASELINE configs[1] at E=5; seeded)",
+            "config": {"workload": f"configs[1] m={m} E={e}: {n} pairs per GPU, 50% planted "
+                                   f"k~U{{0..{2 * e}}} sub/ins/del, 50% independent; ASCII records, "
+                                   f"pitch {pitch}", "m": m, "E": e, "width": 4,
+                       "pairs_per_gpu": n, "global_pairs": n * world,
+                       "parallelism": f"dp{world} (contiguous pair shards, no collective)",
+                       "l2": f"inputs {2 * n * pitch / 1e9:.1f} GB per GPU >> 126 MB L2 (no flush)"},
+            "roofline": roofline, "int_roofline": int_view, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": ck, "clocks_e2e": ck_e2e,
+            "kernel_ms": [round(x, 4) for x in kern_ms],
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

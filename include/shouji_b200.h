@@ -1,0 +1,162 @@
+/*
+ * shouji_b200 — C ABI of the B200-native Shouji pre-alignment filter.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *
+ *   prefilter::shouji_filter(const packed_sequence& pattern,
+ *                            const packed_sequence& text,
+ *                            std::uint32_t e, unsigned width = 4)
+ *       proj/include/prefilter/shouji.hpp:57-59, proj/src/shouji.cpp:41-58
+ *
+ * and of its batch callers (run_filter proj/src/evaluate.cpp:13-21 driven by
+ * parallel_for_pairs proj/src/evaluate.cpp:23-48, run_bench
+ * proj/src/bench.cpp:11-42). Plain pointers and sizes only; no C++ or torch
+ * types cross it. All compute runs in hand-written sm_100a kernels; there is
+ * no CPU fallback: without a usable CUDA device every compute entry point
+ * returns PF_ERR_NO_DEVICE.
+ *
+ * Input records are ASCII (A/C/G/T/N, upper case only — lower case is an
+ * illegal character exactly as in packed_sequence::from_string,
+ * proj/src/packed_sequence.cpp:19-29). Pair i's text (reference segment) is
+ * at text + i*stride and its pattern (read) at pattern + i*stride, m bytes
+ * each. Argument order follows the reference: the PATTERN is the read, the
+ * TEXT the reference segment; swapping them changes results.
+ *
+ * Outputs: accept_bitmap is LSB-first, bit i%32 of word i/32 is pair i's
+ * accept (ceil(n/32) words; bits past n are zero). estimates[i] is the
+ * filter_decision::edit_estimate (popcount of the tally vector,
+ * proj/include/prefilter/filter_decision.hpp:12-16). bits, when requested,
+ * holds the tally vector of pair i as ceil(m/64) LSB-first uint64 words at
+ * bits + i*ceil(m/64) (bitvector word layout, bitvector.hpp:16-31).
+ */
+#ifndef SHOUJI_B200_H
+#define SHOUJI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes map 1:1 onto the reference exception classes
+ * (proj/include/prefilter/errors.hpp:11-84). */
+typedef enum pf_status {
+    PF_OK = 0,
+    PF_ERR_EMPTY_SEQUENCE = 1,      /* empty_sequence_error      errors.hpp:17-20 */
+    PF_ERR_ILLEGAL_CHARACTER = 2,   /* illegal_character_error   errors.hpp:23-37 */
+    PF_ERR_LENGTH_MISMATCH = 3,     /* length_mismatch_error     errors.hpp:40-48 */
+    PF_ERR_THRESHOLD_TOO_LARGE = 4, /* threshold_too_large_error errors.hpp:52-57 */
+    PF_ERR_OUT_OF_BAND = 5,         /* out_of_band_error         errors.hpp:60-65 */
+    PF_ERR_PARSE = 6,               /* parse_error               errors.hpp:68-77 */
+    PF_ERR_INVALID_PARAMETERS = 7,  /* invalid_parameters_error  errors.hpp:81-84 */
+    PF_ERR_NO_DEVICE = 100,         /* no usable sm_100 CUDA device */
+    PF_ERR_CUDA = 101,              /* a CUDA runtime call failed */
+    PF_ERR_OUT_OF_MEMORY = 102,
+    PF_ERR_NULL_ARGUMENT = 103
+} pf_status;
+
+/* Where an error was found. For PF_ERR_ILLEGAL_CHARACTER: the lowest pair
+ * index holding an illegal byte, text (field 0) checked before pattern
+ * (field 1) as load_pairs does (proj/src/dataset.cpp:28-30), and the first
+ * offending offset within that sequence (packed_sequence.cpp:27-28). */
+typedef struct pf_error {
+    int32_t status;
+    uint32_t field;    /* 0 = text, 1 = pattern */
+    uint64_t pair;
+    uint64_t position;
+    uint32_t byte;
+    int32_t cuda_error; /* cudaError_t when status == PF_ERR_CUDA */
+    char message[160];
+} pf_error;
+
+typedef struct pf_ctx pf_ctx;
+
+/* Library / device information. */
+const char* pf_status_string(int status);
+const char* pf_version(void);
+/* Number of CUDA devices usable by this build (0 when none). */
+int pf_device_count(void);
+
+/* Context over a set of devices (one stream, pinned staging and device
+ * buffers per device; all library-owned). A batch is split into contiguous
+ * pair ranges, 32-pair aligned, one per device — the static chunking of
+ * parallel_for_pairs (evaluate.cpp:36-37) — and gathered on the host; there
+ * is no device-to-device traffic. devices == NULL / count == 0 means device 0.
+ * A context is internally serialised; use one per host thread for concurrency. */
+int pf_ctx_create(const int* devices, int count, pf_ctx** out);
+void pf_ctx_destroy(pf_ctx* ctx);
+int pf_ctx_device_count(const pf_ctx* ctx);
+
+/* Batched Shouji over caller-owned HOST buffers (pinned or pageable; pinned
+ * buffers are DMA'd directly). Synchronous. Checks, in the reference's order:
+ *   m == 0 with n > 0                  -> PF_ERR_EMPTY_SEQUENCE
+ *   any illegal byte                   -> PF_ERR_ILLEGAL_CHARACTER (+ err)
+ *   width outside [3, 8]               -> PF_ERR_INVALID_PARAMETERS
+ *   e >= m                             -> every pair accepted, estimate 0,
+ *                                         all-zero bits (shouji.cpp:48-49)
+ * estimates and bits may be NULL. stride >= m. */
+int pf_shouji_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern,
+                           size_t stride, size_t n, uint32_t m, uint32_t e, uint32_t width,
+                           uint32_t* accept_bitmap, uint32_t* estimates, uint64_t* bits,
+                           pf_error* err);
+
+/* Same over DEVICE-resident records on the ctx's first device, asynchronous
+ * on `stream` (a cudaStream_t; NULL = the ctx stream) except that an error
+ * check forces a stream synchronisation at the end. Records must use
+ * pf_device_pitch(m) bytes per row and 16-byte aligned bases (so every row
+ * starts 16-byte aligned); bytes in [m, pitch) are ignored. Output pointers
+ * are device pointers (accept_bitmap ceil(n/32) words; estimates/bits as for
+ * the host call, may be NULL). */
+int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                            size_t pitch, size_t n, uint32_t m, uint32_t e, uint32_t width,
+                            uint32_t* d_accept_bitmap, uint32_t* d_estimates, uint64_t* d_bits,
+                            void* stream, pf_error* err);
+
+/* Same as pf_shouji_filter_device but fully asynchronous: no host sync and no
+ * error location. Any illegal byte ORs 1 into *d_err_flag (a device word the
+ * caller zeroes); call pf_shouji_filter_device to locate it. Used for
+ * back-to-back device-resident throughput runs. e < m and 3 <= width <= 8
+ * are required (the short-circuit / width errors need the synchronous call). */
+int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                                  size_t pitch, size_t n, uint32_t m, uint32_t e, uint32_t width,
+                                  uint32_t* d_accept_bitmap, uint32_t* d_estimates,
+                                  uint32_t* d_err_flag, void* stream);
+
+/* Measured integer pipe throughput on the ctx's first device (diagnostic for
+ * the INT roofline): op 0 = LOP3, 1 = funnel shift, 2 = PRMT, 3 = IMAD.
+ * Writes lane-operations per second. */
+int pf_int_peak(pf_ctx* ctx, int op, double* ops_per_second);
+
+/* Row pitch the device entry point expects for length-m records. */
+size_t pf_device_pitch(uint32_t m);
+
+/* Per-pair compatibility entry (a batch of one), reference argument order:
+ * shouji_filter(pattern, text, e, width). Lengths may differ (->
+ * PF_ERR_LENGTH_MISMATCH, checked before the width, shouji.cpp:44-47).
+ * bits may be NULL (else ceil(text_len/64) words). */
+int pf_shouji_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, const char* text,
+                         size_t text_len, uint32_t e, uint32_t width, int* accept,
+                         uint32_t* estimate, uint64_t* bits, pf_error* err);
+
+/* Pinned host allocation helpers (cudaHostAlloc on the ctx's first device). */
+void* pf_host_alloc(size_t bytes);
+void pf_host_free(void* p);
+
+/* Seeded synthetic pair generator on the device (bench / test workloads; see
+ * DESIGN.md "Synthetic configs"). Writes n records of length m with the
+ * given pitch into d_text / d_pattern. kind: 1..4 = BASELINE.json configs 1..4
+ * (param = E for configs 1 and 3, ignored otherwise). Deterministic in
+ * (kind, seed, param, pair index). */
+int pf_generate_device(pf_ctx* ctx, int kind, uint64_t seed, uint32_t param, uint8_t* d_text,
+                       uint8_t* d_pattern, size_t pitch, size_t n, uint32_t m, void* stream);
+
+/* Number of kernel launches issued by this process so far (all contexts);
+ * bench.py reports the delta over its timed region. */
+uint64_t pf_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHOUJI_B200_H */

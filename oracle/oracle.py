@@ -1,0 +1,228 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes front end for the two CPU checkers.
+
+* ``Oracle``   — the plain-C restatement (oracle/shouji_oracle.c).
+* ``Reference`` — the unmodified reference library compiled from its sources
+  (oracle/_ref/libprefilter_ref.so, built by oracle/Makefile); ``None`` when
+  that build is absent.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's cpu_baseline leg /
+``--impl reference`` arm may import this module. The product package never
+does: its only compute path is the CUDA extension.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "libshouji_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libprefilter_ref.so")
+
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+
+
+class OracleError(Exception):
+    def __init__(self, code, pair=0, field=0, position=0, byte=0):
+        super().__init__(f"oracle status {code} (pair={pair} field={field} pos={position} byte={byte})")
+        self.code, self.pair, self.field, self.position, self.byte = code, pair, field, position, byte
+
+
+class _SoError(C.Structure):
+    _fields_ = [("code", C.c_int), ("pair", C.c_uint64), ("field", C.c_int),
+                ("position", C.c_uint64), ("byte", C.c_int)]
+
+
+def build():
+    """Compile the checkers (make -C oracle). Safe to call repeatedly."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _records(text, pattern):
+    text = np.ascontiguousarray(text, dtype=np.uint8)
+    pattern = np.ascontiguousarray(pattern, dtype=np.uint8)
+    assert text.shape == pattern.shape and text.ndim == 2
+    return text, pattern
+
+
+class Oracle:
+    """The C restatement (see shouji_oracle.c for the reference file:line map)."""
+
+    def __init__(self, path=ORACLE_SO):
+        if not os.path.exists(path):
+            build()
+        lib = C.CDLL(path)
+        lib.so_shouji_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t,
+                                        C.c_uint32, C.c_uint, C.c_uint, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.POINTER(_SoError)]
+        lib.so_shouji_one.argtypes = [C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t, C.c_uint32,
+                                      C.c_uint, C.c_void_p, C.POINTER(C.c_uint32),
+                                      C.POINTER(C.c_int)]
+        lib.so_neighborhood.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, C.c_uint32, C.c_void_p]
+        lib.so_generate_pairs.argtypes = [C.c_uint64, C.c_size_t, C.c_size_t, C.c_uint32,
+                                          C.c_uint32, C.c_void_p, C.c_void_p, C.c_size_t]
+        lib.so_banded_edit_distance.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, C.c_uint32]
+        lib.so_banded_edit_distance.restype = C.c_int32
+        lib.so_set_variant.argtypes = [C.c_int]
+        self.lib = lib
+
+    def set_variant(self, v: int):
+        """Mutation-test knob: 0 reference rules; 1 reverse scan; 2 no leading-zero
+        tie-break; 3 non-strict commit; 4 pattern/text swapped."""
+        self.lib.so_set_variant(v)
+
+    def shouji_batch(self, text, pattern, e, width=4, threads=None, estimates=True, bits=False):
+        """Returns (accept_bitmap u32[ceil(n/32)], estimates u32[n] | None, bits u64[n, W64] | None)."""
+        text, pattern = _records(text, pattern)
+        n, m = text.shape
+        threads = threads or os.cpu_count() or 1
+        acc = np.zeros((n + 31) // 32, np.uint32)
+        est = np.zeros(n, np.uint32) if estimates else None
+        bv = np.zeros((n, (m + 63) // 64), np.uint64) if bits else None
+        err = _SoError()
+        st = self.lib.so_shouji_batch(_ptr(text), _ptr(pattern), m, n, m, e, width, threads,
+                                      _ptr(acc), _ptr(est), _ptr(bv), C.byref(err))
+        if st:
+            raise OracleError(st, err.pair, err.field, err.position, err.byte)
+        return acc, est, bv
+
+    def shouji_one(self, pattern: str, text: str, e: int, width: int = 4):
+        """shouji_filter(seq(pattern), seq(text), e, width) -> (accept, estimate, bits str)."""
+        pb, tb = pattern.encode(), text.encode()
+        bits = np.zeros(max(len(tb), 1), np.uint8)
+        est, acc = C.c_uint32(), C.c_int()
+        st = self.lib.so_shouji_one(pb, len(pb), tb, len(tb), e, width, _ptr(bits),
+                                    C.byref(est), C.byref(acc))
+        if st:
+            raise OracleError(st)
+        return bool(acc.value), est.value, "".join("1" if b else "0" for b in bits[:len(tb)])
+
+    def neighborhood(self, pattern: str, text: str, e: int):
+        """(2e+1, m) uint8 map, row d+e."""
+        m = len(text)
+        out = np.zeros((2 * e + 1, m), np.uint8)
+        self.lib.so_neighborhood(pattern.encode(), text.encode(), m, e, _ptr(out))
+        return out
+
+    def generate_pairs(self, seed, count, length, lo, hi):
+        """Restated generate_pairs -> (text u8[count, length], pattern u8[count, length])."""
+        t = np.zeros((count, length), np.uint8)
+        p = np.zeros((count, length), np.uint8)
+        st = self.lib.so_generate_pairs(seed, count, length, lo, hi, _ptr(t), _ptr(p), length)
+        if st:
+            raise OracleError(st)
+        return t, p
+
+    def banded_edit_distance(self, pattern: bytes, text: bytes, e: int) -> int:
+        return self.lib.so_banded_edit_distance(pattern, text, len(text), e)
+
+
+class Reference:
+    """The unmodified reference library (oracle/_ref/libprefilter_ref.so)."""
+
+    def __init__(self, path=REF_SO):
+        lib = C.CDLL(path)
+        lib.ref_generate_pairs.argtypes = [C.c_uint64, C.c_size_t, C.c_size_t, C.c_uint32,
+                                           C.c_uint32, C.c_void_p, C.c_void_p, C.c_size_t]
+        lib.ref_pack.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t,
+                                 C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.POINTER(C.c_int),
+                                 C.POINTER(C.c_uint64), C.POINTER(C.c_int)]
+        lib.ref_pack.restype = C.c_void_p
+        lib.ref_free.argtypes = [C.c_void_p]
+        lib.ref_shouji_run.argtypes = [C.c_void_p, C.c_uint32, C.c_uint, C.c_uint, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_size_t]
+        lib.ref_magnet_run.argtypes = [C.c_void_p, C.c_uint32, C.c_uint, C.c_void_p, C.c_void_p]
+        lib.ref_banded_run.argtypes = [C.c_void_p, C.c_uint32, C.c_uint, C.c_void_p]
+        lib.ref_shouji_one.argtypes = [C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t, C.c_uint32,
+                                       C.c_uint, C.POINTER(C.c_int), C.POINTER(C.c_uint32),
+                                       C.c_char_p]
+        lib.ref_hardware_concurrency.restype = C.c_uint
+        self.lib = lib
+
+    @staticmethod
+    def available(path=REF_SO):
+        return os.path.exists(path)
+
+    def hardware_concurrency(self):
+        return self.lib.ref_hardware_concurrency()
+
+    def generate_pairs(self, seed, count, length, lo, hi):
+        t = np.zeros((count, length), np.uint8)
+        p = np.zeros((count, length), np.uint8)
+        st = self.lib.ref_generate_pairs(seed, count, length, lo, hi, _ptr(t), _ptr(p), length)
+        if st:
+            raise OracleError(st)
+        return t, p
+
+    def pack(self, text, pattern):
+        """Pack with packed_sequence::from_string; returns a handle (free with .free)."""
+        text, pattern = _records(text, pattern)
+        n, m = text.shape
+        code, pair, field, pos, byte = C.c_int(), C.c_uint64(), C.c_int(), C.c_uint64(), C.c_int()
+        h = self.lib.ref_pack(_ptr(text), _ptr(pattern), m, n, m, C.byref(code), C.byref(pair),
+                              C.byref(field), C.byref(pos), C.byref(byte))
+        if not h:
+            raise OracleError(code.value, pair.value, field.value, pos.value, byte.value)
+        return _Packed(self, h, n, m)
+
+    def shouji_batch(self, text, pattern, e, width=4, threads=None, estimates=True, bits=False):
+        packed = self.pack(text, pattern)
+        try:
+            return packed.shouji(e, width, threads, estimates, bits)
+        finally:
+            packed.free()
+
+    def shouji_one(self, pattern: str, text: str, e: int, width: int = 4):
+        pb, tb = pattern.encode(), text.encode()
+        acc, est = C.c_int(), C.c_uint32()
+        buf = C.create_string_buffer(len(tb) + 1)
+        st = self.lib.ref_shouji_one(pb, len(pb), tb, len(tb), e, width, C.byref(acc),
+                                     C.byref(est), buf)
+        if st:
+            raise OracleError(st)
+        return bool(acc.value), est.value, buf.value.decode()
+
+
+class _Packed:
+    def __init__(self, ref, handle, n, m):
+        self.ref, self.h, self.n, self.m = ref, handle, n, m
+
+    def shouji(self, e, width=4, threads=None, estimates=True, bits=False):
+        threads = threads or self.ref.hardware_concurrency() or 1
+        acc = np.zeros((self.n + 31) // 32, np.uint32)
+        est = np.zeros(self.n, np.uint32) if estimates else None
+        wpp = (self.m + 63) // 64
+        bv = np.zeros((self.n, wpp), np.uint64) if bits else None
+        st = self.ref.lib.ref_shouji_run(self.h, e, width, threads, _ptr(acc), _ptr(est),
+                                         _ptr(bv), wpp)
+        if st:
+            raise OracleError(st)
+        return acc, est, bv
+
+    def magnet(self, e, threads=None):
+        threads = threads or self.ref.hardware_concurrency() or 1
+        acc = np.zeros((self.n + 31) // 32, np.uint32)
+        est = np.zeros(self.n, np.uint32)
+        st = self.ref.lib.ref_magnet_run(self.h, e, threads, _ptr(acc), _ptr(est))
+        if st:
+            raise OracleError(st)
+        return acc, est
+
+    def banded(self, e, threads=None):
+        threads = threads or self.ref.hardware_concurrency() or 1
+        out = np.zeros(self.n, np.int32)
+        st = self.ref.lib.ref_banded_run(self.h, e, threads, _ptr(out))
+        if st:
+            raise OracleError(st)
+        return out
+
+    def free(self):
+        if self.h:
+            self.ref.lib.ref_free(self.h)
+            self.h = None

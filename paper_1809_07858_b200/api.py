@@ -1,0 +1,374 @@
+"""Python mirror of the reference's public interface for the Shouji path.
+
+Names, argument meaning and error behaviour follow ``prefilter`` (C++,
+/root/reference/proj/include/prefilter/): ``packed_sequence``, ``bitvector``,
+``filter_decision``, ``shouji_filter(pattern, text, e, width=4)``, ``run_filter``
+and the ``error`` hierarchy of errors.hpp. Every decision is computed by the
+sm_100a kernels behind the C ABI (libshouji_b200.so); this module only moves
+buffers and maps status codes onto exceptions.
+
+Batch entry points (``shouji_filter_batch``, ``shouji_filter_device``) are the
+fast path: they take N equal-length ASCII records at once, which is how the
+reference's callers (evaluate, run_bench, the CLI) drive the filter through
+parallel_for_pairs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+default_window_width = 4
+min_window_width = 3
+max_window_width = 8
+
+
+# ---------------------------------------------------------------------------
+# Errors (proj/include/prefilter/errors.hpp:11-84)
+# ---------------------------------------------------------------------------
+class error(RuntimeError):
+    """Base of every recoverable error (prefilter::error)."""
+
+
+class empty_sequence_error(error):
+    def __init__(self, msg="empty sequence"):
+        super().__init__(msg)
+
+
+class illegal_character_error(error):
+    def __init__(self, position: int, byte: int, pair: int | None = None, field: int | None = None):
+        ch = chr(byte) if 32 <= byte < 127 else f"\\x{byte:02x}"
+        where = "" if pair is None else f" of {'text' if field == 0 else 'pattern'} {pair}"
+        super().__init__(f"illegal character '{ch}' at position {position}{where}")
+        self._position, self._byte, self.pair, self.field = position, byte, pair, field
+
+    def position(self) -> int:
+        return self._position
+
+    def byte(self) -> str:
+        return chr(self._byte)
+
+
+class length_mismatch_error(error):
+    pass
+
+
+class threshold_too_large_error(error):
+    pass
+
+
+class out_of_band_error(error):
+    pass
+
+
+class parse_error(error):
+    def __init__(self, line: int, reason: str):
+        super().__init__(f"line {line}: {reason}")
+        self._line = line
+
+    def line(self) -> int:
+        return self._line
+
+
+class invalid_parameters_error(error):
+    pass
+
+
+class device_error(RuntimeError):
+    """No usable sm_100 device, or a CUDA failure (not a reference error class)."""
+
+
+def _raise(status: int, err: L.PfError | None = None):
+    if status == L.PF_OK:
+        return
+    msg = err.message.decode(errors="replace") if err is not None else L.lib.pf_status_string(status).decode()
+    if status == L.PF_ERR_EMPTY_SEQUENCE:
+        raise empty_sequence_error()
+    if status == L.PF_ERR_ILLEGAL_CHARACTER:
+        raise illegal_character_error(int(err.position), int(err.byte), int(err.pair), int(err.field))
+    if status == L.PF_ERR_LENGTH_MISMATCH:
+        raise length_mismatch_error(msg)
+    if status == L.PF_ERR_THRESHOLD_TOO_LARGE:
+        raise threshold_too_large_error(msg)
+    if status == L.PF_ERR_OUT_OF_BAND:
+        raise out_of_band_error(msg)
+    if status == L.PF_ERR_INVALID_PARAMETERS:
+        raise invalid_parameters_error(msg)
+    raise device_error(f"{L.lib.pf_status_string(status).decode()}: {msg}")
+
+
+# ---------------------------------------------------------------------------
+# Containers (bitvector.hpp, packed_sequence.hpp, filter_decision.hpp)
+# ---------------------------------------------------------------------------
+class bitvector:
+    """Fixed-length LSB-first bit sequence in uint64 words (bitvector.hpp:16-129)."""
+
+    def __init__(self, nbits: int = 0, value: bool = False, words=None):
+        self._n = int(nbits)
+        nw = (self._n + 63) // 64
+        if words is None:
+            self._w = np.full(nw, np.uint64(0xFFFFFFFFFFFFFFFF) if value else 0, np.uint64)
+        else:
+            self._w = np.array(words, dtype=np.uint64).reshape(-1)[:nw].copy()
+        if self._n & 63 and nw:
+            self._w[-1] &= np.uint64((1 << (self._n & 63)) - 1)
+
+    def size(self) -> int:
+        return self._n
+
+    def get(self, i: int) -> bool:
+        return bool((int(self._w[i >> 6]) >> (i & 63)) & 1)
+
+    def count_ones(self) -> int:
+        return int(sum(bin(int(w)).count("1") for w in self._w))
+
+    def count_zeros(self) -> int:
+        return self._n - self.count_ones()
+
+    def words(self):
+        return self._w
+
+    def to_string(self) -> str:
+        return "".join("1" if self.get(i) else "0" for i in range(self._n))
+
+    def __eq__(self, other):
+        return isinstance(other, bitvector) and self._n == other._n and bool((self._w == other._w).all())
+
+    def __repr__(self):
+        return f"bitvector({self.to_string()!r})"
+
+
+class packed_sequence:
+    """A validated A/C/G/T/N sequence (packed_sequence.hpp:17-54).
+
+    ``from_string`` enforces the reference codec's contract (upper case only;
+    empty -> empty_sequence_error; first bad byte -> illegal_character_error with
+    its 0-based position). The planes themselves are built on the device by the
+    filter kernels from the ASCII bytes kept here.
+    """
+
+    __slots__ = ("_ascii",)
+
+    def __init__(self, ascii_bytes: bytes = b""):
+        self._ascii = ascii_bytes
+
+    @staticmethod
+    def from_string(raw) -> "packed_sequence":
+        b = raw.encode() if isinstance(raw, str) else bytes(raw)
+        if len(b) == 0:
+            raise empty_sequence_error()
+        arr = np.frombuffer(b, np.uint8)
+        ok = np.isin(arr, np.frombuffer(b"ACGTN", np.uint8))
+        if not ok.all():
+            pos = int(np.argmin(ok))
+            raise illegal_character_error(pos, int(arr[pos]))
+        return packed_sequence(b)
+
+    def to_string(self) -> str:
+        return self._ascii.decode()
+
+    def ascii(self) -> bytes:
+        return self._ascii
+
+    def size(self) -> int:
+        return len(self._ascii)
+
+    def is_n(self, i: int) -> bool:
+        return self._ascii[i] == ord("N")
+
+    def code(self, i: int) -> int:
+        return {ord("A"): 0, ord("C"): 1, ord("G"): 2, ord("T"): 3}.get(self._ascii[i], 0)
+
+    def base_at(self, i: int) -> str:
+        return chr(self._ascii[i])
+
+    def __eq__(self, other):
+        return isinstance(other, packed_sequence) and self._ascii == other._ascii
+
+    def __len__(self):
+        return len(self._ascii)
+
+
+def seq(s) -> packed_sequence:
+    """Test shorthand, as in proj/tests/helpers.hpp:17-19."""
+    return packed_sequence.from_string(s)
+
+
+@dataclass
+class filter_decision:
+    """Outcome of one filter run (filter_decision.hpp:12-16)."""
+    accept: bool = False
+    edit_estimate: int = 0
+    bits: bitvector = field(default_factory=bitvector)
+
+
+# ---------------------------------------------------------------------------
+# Device context
+# ---------------------------------------------------------------------------
+class Context:
+    """A set of devices the batch calls are sharded across (pf_ctx)."""
+
+    def __init__(self, devices: Sequence[int] | None = None):
+        self._h = C.c_void_p()
+        if devices:
+            arr = (C.c_int * len(devices))(*devices)
+            st = L.lib.pf_ctx_create(arr, len(devices), C.byref(self._h))
+        else:
+            st = L.lib.pf_ctx_create(None, 0, C.byref(self._h))
+        _raise(st)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def device_count(self) -> int:
+        return L.lib.pf_ctx_device_count(self._h)
+
+    def close(self):
+        if self._h:
+            L.lib.pf_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Context | None = None
+_ctx_lock = threading.Lock()
+
+
+def default_context() -> Context:
+    global _default_ctx
+    with _ctx_lock:
+        if _default_ctx is None:
+            _default_ctx = Context()
+        return _default_ctx
+
+
+def device_count() -> int:
+    return L.lib.pf_device_count()
+
+
+def launch_count() -> int:
+    """Kernel launches issued by this process (all contexts)."""
+    return int(L.lib.pf_launch_count())
+
+
+def device_pitch(m: int) -> int:
+    return int(L.lib.pf_device_pitch(m))
+
+
+# ---------------------------------------------------------------------------
+# Filter entry points
+# ---------------------------------------------------------------------------
+def shouji_filter(pattern: packed_sequence, text: packed_sequence, e: int,
+                  width: int = default_window_width, ctx: Context | None = None) -> filter_decision:
+    """shouji_filter(pattern=read, text=reference segment, e, width) — shouji.hpp:57-59.
+
+    Raises length_mismatch_error, then invalid_parameters_error (width), in the
+    reference's order (shouji.cpp:44-47); e >= m accepts with estimate 0.
+    """
+    ctx = ctx or default_context()
+    pb, tb = pattern.ascii(), text.ascii()
+    acc, est = C.c_int(), C.c_uint32()
+    nbits = len(tb)
+    words = np.zeros(max((nbits + 63) // 64, 1), np.uint64)
+    err = L.PfError()
+    st = L.lib.pf_shouji_filter_one(ctx.handle, pb, len(pb), tb, len(tb), int(e), int(width),
+                                    C.byref(acc), C.byref(est), words.ctypes.data_as(C.c_void_p),
+                                    C.byref(err))
+    _raise(st, err)
+    return filter_decision(bool(acc.value), int(est.value), bitvector(nbits, words=words))
+
+
+def run_filter(algo: str, pattern: packed_sequence, text: packed_sequence, e: int,
+               width: int = default_window_width) -> filter_decision:
+    """run_filter (evaluate.cpp:13-21) for the path this framework accelerates."""
+    if algo != "shouji":
+        raise invalid_parameters_error(f"filter '{algo}' is outside this framework's scope")
+    return shouji_filter(pattern, text, e, width)
+
+
+def _as_records(x, m=None):
+    a = np.ascontiguousarray(x, dtype=np.uint8)
+    if a.ndim != 2:
+        raise invalid_parameters_error("records must be a 2-D uint8 array [n, stride]")
+    return a
+
+
+def shouji_filter_batch(text, pattern, e: int, width: int = default_window_width, m: int | None = None,
+                        estimates: bool = False, bits: bool = False, ctx: Context | None = None):
+    """Filter N pairs of host ASCII records; text[i] is pair i's reference
+    segment, pattern[i] its read (uint8 arrays [n, stride], first m bytes used).
+
+    Returns (accept_bitmap u32[ceil(n/32)], estimates u32[n] | None, bits u64[n, ceil(m/64)] | None).
+    """
+    ctx = ctx or default_context()
+    text = _as_records(text)
+    pattern = _as_records(pattern)
+    if text.shape != pattern.shape:
+        raise length_mismatch_error("text and pattern record arrays differ in shape")
+    n, stride = text.shape
+    m = stride if m is None else int(m)
+    acc = np.zeros((n + 31) // 32, np.uint32)
+    est = np.zeros(n, np.uint32) if estimates else None
+    bv = np.zeros((n, (m + 63) // 64), np.uint64) if bits else None
+    err = L.PfError()
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p) if a is not None else None  # noqa: E731
+    st = L.lib.pf_shouji_filter_batch(ctx.handle, ptr(text), ptr(pattern), stride, n, m, int(e),
+                                      int(width), ptr(acc), ptr(est), ptr(bv), C.byref(err))
+    _raise(st, err)
+    return acc, est, bv
+
+
+def shouji_filter_device(d_text: int, d_pattern: int, pitch: int, n: int, m: int, e: int,
+                         d_accept: int, width: int = default_window_width, d_estimates: int | None = None,
+                         d_bits: int | None = None, stream: int | None = None,
+                         ctx: Context | None = None) -> None:
+    """Device-resident batch (raw device pointers, e.g. torch ``data_ptr()``)."""
+    ctx = ctx or default_context()
+    err = L.PfError()
+    st = L.lib.pf_shouji_filter_device(ctx.handle, d_text, d_pattern, pitch, n, m, int(e), int(width),
+                                       d_accept, d_estimates, d_bits, stream, C.byref(err))
+    _raise(st, err)
+
+
+def generate_device(kind: int, seed: int, param: int, d_text: int, d_pattern: int, pitch: int,
+                    n: int, m: int, stream: int | None = None, ctx: Context | None = None) -> None:
+    """Seeded synthetic pairs for BASELINE configs 1-4, written on the device."""
+    ctx = ctx or default_context()
+    _raise(L.lib.pf_generate_device(ctx.handle, kind, seed, param, d_text, d_pattern, pitch, n, m,
+                                    stream))
+
+
+def unpack_bitmap(bitmap: np.ndarray, n: int) -> np.ndarray:
+    """LSB-first u32 bitmap -> bool[n]."""
+    b = np.unpackbits(np.ascontiguousarray(bitmap, np.uint32).view(np.uint8), bitorder="little")
+    return b[:n].astype(bool)
+
+
+def shouji_filter_device_async(d_text: int, d_pattern: int, pitch: int, n: int, m: int, e: int,
+                               d_accept: int, d_err_flag: int, width: int = default_window_width,
+                               d_estimates: int | None = None, stream: int | None = None,
+                               ctx: Context | None = None) -> None:
+    """Asynchronous device-resident batch: no host sync; illegal bytes only set *d_err_flag."""
+    ctx = ctx or default_context()
+    _raise(L.lib.pf_shouji_filter_device_async(ctx.handle, d_text, d_pattern, pitch, n, m, int(e),
+                                               int(width), d_accept, d_estimates, d_err_flag, stream))
+
+
+def int_peak(op: str = "lop3", ctx: Context | None = None) -> float:
+    """Measured integer lane-ops/s of one instruction class on the ctx's device."""
+    ctx = ctx or default_context()
+    code = {"lop3": 0, "shf": 1, "prmt": 2, "imad": 3}[op]
+    out = C.c_double()
+    _raise(L.lib.pf_int_peak(ctx.handle, code, C.byref(out)))
+    return out.value

@@ -1,0 +1,633 @@
+// C ABI of the B200-native Shouji filter (declared in include/shouji_b200.h).
+//
+// Host side of the boundary: argument checks in the reference's order
+// (proj/src/shouji.cpp:44-49, packed_sequence.cpp:8,27-28), device buffer and
+// pinned-staging management, the 32-pair-aligned static split across devices
+// (the contiguous chunking of parallel_for_pairs, proj/src/evaluate.cpp:36-37)
+// and the gather of per-device bitmaps. No compute happens here: every pair
+// goes through the sm_100a kernels in kernels.cu; without a device the calls
+// fail with PF_ERR_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "../../include/shouji_b200.h"
+#include "kernels.cuh"
+
+namespace {
+
+constexpr size_t kStageRows = 1 << 18;  // pairs per pinned staging chunk (pageable input)
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct DeviceState {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint8_t* d_text = nullptr;
+    uint8_t* d_pattern = nullptr;
+    size_t in_bytes = 0;
+    size_t in_pattern_bytes = 0;
+    uint32_t* d_accept = nullptr;
+    size_t accept_words = 0;
+    uint32_t* d_est = nullptr;
+    size_t est_n = 0;
+    uint64_t* d_bits = nullptr;
+    size_t bits_words = 0;
+    uint32_t* d_outplanes = nullptr;
+    size_t outplanes_words = 0;
+    uint32_t* d_scratch = nullptr;
+    size_t scratch_words = 0;
+    uint32_t* d_flag = nullptr;
+    unsigned long long* d_key = nullptr;
+    uint8_t* h_stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+};
+
+}  // namespace
+
+struct pf_ctx {
+    std::vector<DeviceState> devs;
+    std::mutex mu;
+};
+
+namespace {
+
+void set_err(pf_error* err, int status, const char* msg, cudaError_t ce = cudaSuccess) {
+    if (!err) return;
+    err->status = status;
+    err->cuda_error = static_cast<int32_t>(ce);
+    if (msg) {
+        std::snprintf(err->message, sizeof(err->message), "%s%s%s", msg,
+                      ce != cudaSuccess ? ": " : "", ce != cudaSuccess ? cudaGetErrorString(ce) : "");
+    }
+}
+
+#define PF_CUDA(call)                                                  \
+    do {                                                               \
+        cudaError_t ce_ = (call);                                      \
+        if (ce_ != cudaSuccess) {                                      \
+            set_err(err, ce_ == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA, \
+                    #call, ce_);                                       \
+            return ce_ == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA; \
+        }                                                              \
+    } while (0)
+
+template <typename T>
+cudaError_t grow(T*& p, size_t& have, size_t need) {
+    if (need <= have && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    have = 0;
+    const size_t n = std::max<size_t>(need, 1);
+    cudaError_t st = cudaMalloc(&p, n * sizeof(T));
+    if (st == cudaSuccess) have = n;
+    return st;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Decode the locator key and fill err (the byte is read from the records).
+void decode_illegal(unsigned long long key, long long pair_base, const uint8_t* text,
+                    const uint8_t* pattern, size_t stride, bool host_records, pf_error* err) {
+    const unsigned long long pf = key >> 24;
+    const uint64_t pair = pf / 2;
+    const uint32_t field = static_cast<uint32_t>(pf % 2);
+    const uint64_t pos = key & 0xFFFFFFull;
+    uint8_t byte = 0;
+    const uint8_t* src = (field == 0 ? text : pattern) + pair * stride + pos;
+    if (host_records)
+        byte = *src;
+    else
+        cudaMemcpy(&byte, src, 1, cudaMemcpyDeviceToHost);
+    if (err) {
+        err->status = PF_ERR_ILLEGAL_CHARACTER;
+        err->pair = pair + static_cast<uint64_t>(pair_base);
+        err->field = field;
+        err->position = pos;
+        err->byte = byte;
+        std::snprintf(err->message, sizeof(err->message),
+                      "illegal character '%c' at position %llu of %s %llu",
+                      (byte >= 32 && byte < 127) ? byte : '?', (unsigned long long)pos,
+                      field == 0 ? "text" : "pattern", (unsigned long long)err->pair);
+    }
+}
+
+struct ShardResult {
+    int status = PF_OK;
+    pf_error err{};
+};
+
+// Filter pairs [p0, p1) of host records on one device.
+void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern, size_t stride,
+                    size_t p0, size_t p1, uint32_t m, uint32_t e, uint32_t width,
+                    uint32_t* accept_bitmap, uint32_t* estimates, uint64_t* bits,
+                    ShardResult* res) {
+    pf_error* err = &res->err;
+    auto fail = [&](int st) { res->status = st; };
+    const size_t n = p1 - p0;
+    if (n == 0) return;
+    if (cudaSetDevice(d.device) != cudaSuccess) return fail(PF_ERR_NO_DEVICE);
+    const size_t pitch = pf_device_pitch(m);
+    auto cu = [&](cudaError_t ce, const char* what) {
+        if (ce == cudaSuccess) return true;
+        set_err(err, ce == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA, what, ce);
+        fail(ce == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA);
+        return false;
+    };
+    if (!cu(grow(d.d_text, d.in_bytes, n * pitch), "alloc text")) return;
+    if (!cu(grow(d.d_pattern, d.in_pattern_bytes, n * pitch), "alloc pattern")) return;
+    const size_t ngroups = (n + 31) / 32;
+    if (!cu(grow(d.d_accept, d.accept_words, ngroups), "alloc accept")) return;
+    if (estimates && !cu(grow(d.d_est, d.est_n, n), "alloc estimates")) return;
+    const size_t wpp = (m + 63) / 64;
+    if (bits) {
+        if (!cu(grow(d.d_bits, d.bits_words, n * wpp), "alloc bits")) return;
+        if (!cu(grow(d.d_outplanes, d.outplanes_words, size_t(m) * ngroups), "alloc tally planes"))
+            return;
+    }
+    const bool fused = sb::use_fused(width, e, static_cast<int>(m));
+    if (!fused && e < m && width >= 3 && width <= 8) {
+        const size_t need = sb::generic_scratch_words(static_cast<long long>(n), static_cast<int>(m));
+        if (!cu(grow(d.d_scratch, d.scratch_words, need), "alloc scratch")) return;
+    }
+    if (!d.d_flag) {
+        if (!cu(cudaMalloc(&d.d_flag, sizeof(uint32_t)), "alloc flag")) return;
+        if (!cu(cudaMalloc(&d.d_key, sizeof(unsigned long long)), "alloc key")) return;
+    }
+
+    // ---- host -> device ----------------------------------------------------
+    const uint8_t* tsrc = text + p0 * stride;
+    const uint8_t* psrc = pattern + p0 * stride;
+    if (is_pinned(text) && is_pinned(pattern)) {
+        if (!cu(cudaMemcpy2DAsync(d.d_text, pitch, tsrc, stride, m, n, cudaMemcpyHostToDevice,
+                                  d.stream), "H2D text"))
+            return;
+        if (!cu(cudaMemcpy2DAsync(d.d_pattern, pitch, psrc, stride, m, n, cudaMemcpyHostToDevice,
+                                  d.stream), "H2D pattern"))
+            return;
+    } else {
+        // pageable: double-buffered pinned staging, host copy of chunk i+1
+        // overlaps the DMA of chunk i.
+        const size_t rows = std::min(n, kStageRows);
+        const size_t need = rows * m * 2;
+        if (d.stage_bytes < need) {
+            for (int b = 0; b < 2; ++b) {
+                if (d.h_stage[b]) cudaFreeHost(d.h_stage[b]);
+                d.h_stage[b] = nullptr;
+                if (!cu(cudaHostAlloc(&d.h_stage[b], need, cudaHostAllocPortable), "alloc stage"))
+                    return;
+                if (!d.stage_ev[b] &&
+                    !cu(cudaEventCreateWithFlags(&d.stage_ev[b], cudaEventDisableTiming), "event"))
+                    return;
+            }
+            d.stage_bytes = need;
+        }
+        int buf = 0;
+        for (size_t r0 = 0; r0 < n; r0 += rows, buf ^= 1) {
+            const size_t nr = std::min(rows, n - r0);
+            if (!cu(cudaEventSynchronize(d.stage_ev[buf]), "stage wait")) return;
+            uint8_t* st = d.h_stage[buf];
+            uint8_t* sp = st + rows * m;
+            for (size_t r = 0; r < nr; ++r) {
+                std::memcpy(st + r * m, tsrc + (r0 + r) * stride, m);
+                std::memcpy(sp + r * m, psrc + (r0 + r) * stride, m);
+            }
+            if (!cu(cudaMemcpy2DAsync(d.d_text + r0 * pitch, pitch, st, m, m, nr,
+                                      cudaMemcpyHostToDevice, d.stream), "H2D text"))
+                return;
+            if (!cu(cudaMemcpy2DAsync(d.d_pattern + r0 * pitch, pitch, sp, m, m, nr,
+                                      cudaMemcpyHostToDevice, d.stream), "H2D pattern"))
+                return;
+            if (!cu(cudaEventRecord(d.stage_ev[buf], d.stream), "stage record")) return;
+        }
+    }
+
+    // ---- kernels -----------------------------------------------------------
+    if (!cu(cudaMemsetAsync(d.d_flag, 0, sizeof(uint32_t), d.stream), "memset flag")) return;
+    sb::FilterArgs a{};
+    a.text = d.d_text;
+    a.pattern = d.d_pattern;
+    a.pitch = pitch;
+    a.n = static_cast<long long>(n);
+    a.m = static_cast<int>(m);
+    a.e = e;
+    a.width = width;
+    a.accept = d.d_accept;
+    a.estimates = estimates ? d.d_est : nullptr;
+    a.outplanes = bits ? d.d_outplanes : nullptr;
+    a.err_flag = d.d_flag;
+    a.scratch = d.d_scratch;
+    a.scratch_words = d.scratch_words;
+    const bool short_circuit = e >= m;
+    const bool bad_width = width < 3 || width > 8;
+    if (short_circuit || bad_width) {
+        if (!cu(sb::launch_validate(a, d.stream), "validate")) return;
+    } else {
+        if (!cu(sb::launch_filter(a, d.stream), "filter kernel")) return;
+    }
+    uint32_t flag = 0;
+    if (!cu(cudaMemcpyAsync(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, d.stream),
+            "D2H flag"))
+        return;
+    if (!cu(cudaStreamSynchronize(d.stream), "sync")) return;
+    if (flag) {
+        const unsigned long long init = ~0ull;
+        if (!cu(cudaMemcpy(d.d_key, &init, sizeof(init), cudaMemcpyHostToDevice), "key init")) return;
+        if (!cu(sb::launch_locate(d.d_text, d.d_pattern, pitch, a.n, a.m, d.d_key, d.stream),
+                "locate"))
+            return;
+        unsigned long long key = 0;
+        if (!cu(cudaMemcpyAsync(&key, d.d_key, sizeof(key), cudaMemcpyDeviceToHost, d.stream),
+                "D2H key"))
+            return;
+        if (!cu(cudaStreamSynchronize(d.stream), "sync")) return;
+        decode_illegal(key, static_cast<long long>(p0), tsrc, psrc, stride, true, err);
+        return fail(PF_ERR_ILLEGAL_CHARACTER);
+    }
+    if (bad_width) return;  // caller reports invalid parameters after all shards validated
+    if (short_circuit) {
+        if (!cu(sb::launch_accept_all(a.n, a.m, d.d_accept, estimates ? d.d_est : nullptr,
+                                      bits ? d.d_bits : nullptr, d.stream),
+                "accept_all"))
+            return;
+    } else if (bits) {
+        if (!cu(sb::launch_bits_transpose(d.d_outplanes, a.n, a.m, d.d_bits, d.stream), "bits"))
+            return;
+    }
+
+    // ---- device -> host ------------------------------------------------------
+    if (!cu(cudaMemcpyAsync(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, d.stream), "D2H accept"))
+        return;
+    if (estimates &&
+        !cu(cudaMemcpyAsync(estimates + p0, d.d_est, n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                            d.stream), "D2H estimates"))
+        return;
+    if (bits &&
+        !cu(cudaMemcpyAsync(bits + p0 * wpp, d.d_bits, n * wpp * sizeof(uint64_t),
+                            cudaMemcpyDeviceToHost, d.stream), "D2H bits"))
+        return;
+    cu(cudaStreamSynchronize(d.stream), "sync");
+}
+
+const char* kStatusNames[] = {"ok", "empty sequence", "illegal character", "length mismatch",
+                              "threshold too large", "out of band", "parse error",
+                              "invalid parameters"};
+
+}  // namespace
+
+extern "C" {
+
+const char* pf_status_string(int status) {
+    if (status >= 0 && status <= 7) return kStatusNames[status];
+    switch (status) {
+        case PF_ERR_NO_DEVICE: return "no usable CUDA device";
+        case PF_ERR_CUDA: return "CUDA error";
+        case PF_ERR_OUT_OF_MEMORY: return "out of memory";
+        case PF_ERR_NULL_ARGUMENT: return "null argument";
+        default: return "unknown status";
+    }
+}
+
+const char* pf_version(void) { return "shouji_b200 0.1 (sm_100a)"; }
+
+int pf_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+size_t pf_device_pitch(uint32_t m) { return round_up(std::max<uint32_t>(m, 1), 16); }
+
+uint64_t pf_launch_count(void) { return sb::launch_count(); }
+
+int pf_ctx_create(const int* devices, int count, pf_ctx** out) {
+    if (!out) return PF_ERR_NULL_ARGUMENT;
+    *out = nullptr;
+    const int ndev = pf_device_count();
+    if (ndev <= 0) return PF_ERR_NO_DEVICE;
+    std::vector<int> ids;
+    if (!devices || count <= 0)
+        ids.push_back(0);
+    else
+        ids.assign(devices, devices + count);
+    auto* ctx = new pf_ctx;
+    for (int id : ids) {
+        if (id < 0 || id >= ndev) {
+            pf_ctx_destroy(ctx);
+            return PF_ERR_NO_DEVICE;
+        }
+        DeviceState d;
+        d.device = id;
+        if (cudaSetDevice(id) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            pf_ctx_destroy(ctx);
+            return PF_ERR_NO_DEVICE;
+        }
+        cudaDeviceProp prop{};
+        cudaGetDeviceProperties(&prop, id);
+        if (prop.major < 10) {  // kernels are built for sm_100a only
+            cudaStreamDestroy(d.stream);
+            pf_ctx_destroy(ctx);
+            return PF_ERR_NO_DEVICE;
+        }
+        ctx->devs.push_back(d);
+    }
+    *out = ctx;
+    return PF_OK;
+}
+
+void pf_ctx_destroy(pf_ctx* ctx) {
+    if (!ctx) return;
+    for (auto& d : ctx->devs) {
+        cudaSetDevice(d.device);
+        if (d.stream) cudaStreamSynchronize(d.stream);
+        cudaFree(d.d_text);
+        cudaFree(d.d_pattern);
+        cudaFree(d.d_accept);
+        cudaFree(d.d_est);
+        cudaFree(d.d_bits);
+        cudaFree(d.d_outplanes);
+        cudaFree(d.d_scratch);
+        cudaFree(d.d_flag);
+        cudaFree(d.d_key);
+        for (int b = 0; b < 2; ++b) {
+            if (d.h_stage[b]) cudaFreeHost(d.h_stage[b]);
+            if (d.stage_ev[b]) cudaEventDestroy(d.stage_ev[b]);
+        }
+        if (d.stream) cudaStreamDestroy(d.stream);
+    }
+    delete ctx;
+}
+
+int pf_ctx_device_count(const pf_ctx* ctx) { return ctx ? static_cast<int>(ctx->devs.size()) : 0; }
+
+int pf_shouji_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t stride,
+                           size_t n, uint32_t m, uint32_t e, uint32_t width,
+                           uint32_t* accept_bitmap, uint32_t* estimates, uint64_t* bits,
+                           pf_error* err) {
+    if (err) std::memset(err, 0, sizeof(*err));
+    if (!ctx) return PF_ERR_NULL_ARGUMENT;
+    if (n == 0) return PF_OK;
+    if (!text || !pattern || !accept_bitmap) return PF_ERR_NULL_ARGUMENT;
+    if (m == 0) {  // packed_sequence::from_string("") (packed_sequence.cpp:8)
+        set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
+        return PF_ERR_EMPTY_SEQUENCE;
+    }
+    if (stride < m || m >= (1u << 24)) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS, "stride < m or m >= 2^24");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    const size_t nd = ctx->devs.size();
+    // contiguous 32-aligned shards (parallel_for_pairs' n*t/T split, evaluate.cpp:36-37)
+    const size_t groups = (n + 31) / 32;
+    std::vector<size_t> bounds(nd + 1);
+    for (size_t t = 0; t <= nd; ++t) bounds[t] = std::min(n, groups * t / nd * 32);
+    std::vector<ShardResult> res(nd);
+    if (nd == 1) {
+        run_host_shard(ctx->devs[0], text, pattern, stride, bounds[0], bounds[1], m, e, width,
+                       accept_bitmap, estimates, bits, &res[0]);
+    } else {
+        std::vector<std::thread> pool;
+        for (size_t t = 0; t < nd; ++t)
+            pool.emplace_back(run_host_shard, std::ref(ctx->devs[t]), text, pattern, stride,
+                              bounds[t], bounds[t + 1], m, e, width, accept_bitmap, estimates, bits,
+                              &res[t]);
+        for (auto& th : pool) th.join();
+    }
+    // First failure in pair order wins (illegal characters are located per
+    // shard; shards are in pair order).
+    for (size_t t = 0; t < nd; ++t) {
+        if (res[t].status != PF_OK) {
+            if (err) *err = res[t].err;
+            if (err) err->status = res[t].status;
+            return res[t].status;
+        }
+    }
+    if (width < 3 || width > 8) {  // window_zero_table ctor (shouji.cpp:9-15)
+        set_err(err, PF_ERR_INVALID_PARAMETERS, "window width must be in [3, 8]");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    return PF_OK;
+}
+
+int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                            size_t pitch, size_t n, uint32_t m, uint32_t e, uint32_t width,
+                            uint32_t* d_accept_bitmap, uint32_t* d_estimates, uint64_t* d_bits,
+                            void* stream, pf_error* err) {
+    if (err) std::memset(err, 0, sizeof(*err));
+    if (!ctx) return PF_ERR_NULL_ARGUMENT;
+    if (n == 0) return PF_OK;
+    if (!d_text || !d_pattern || !d_accept_bitmap) return PF_ERR_NULL_ARGUMENT;
+    if (m == 0) {
+        set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
+        return PF_ERR_EMPTY_SEQUENCE;
+    }
+    if (pitch % 16 != 0 || pitch < pf_device_pitch(m) ||
+        (reinterpret_cast<uintptr_t>(d_text) | reinterpret_cast<uintptr_t>(d_pattern)) % 16 != 0 ||
+        m >= (1u << 24)) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS,
+                "device records need 16-byte aligned bases and pitch % 16 == 0, pitch >= round16(m)");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceState& d = ctx->devs[0];
+    PF_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    const size_t ngroups = (n + 31) / 32;
+    if (!d.d_flag) {
+        PF_CUDA(cudaMalloc(&d.d_flag, sizeof(uint32_t)));
+        PF_CUDA(cudaMalloc(&d.d_key, sizeof(unsigned long long)));
+    }
+    const bool fused = sb::use_fused(width, e, static_cast<int>(m));
+    if (!fused && e < m && width >= 3 && width <= 8)
+        PF_CUDA(grow(d.d_scratch, d.scratch_words,
+                     sb::generic_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
+    if (d_bits) PF_CUDA(grow(d.d_outplanes, d.outplanes_words, size_t(m) * ngroups));
+    PF_CUDA(cudaMemsetAsync(d.d_flag, 0, sizeof(uint32_t), s));
+    sb::FilterArgs a{};
+    a.text = d_text;
+    a.pattern = d_pattern;
+    a.pitch = pitch;
+    a.n = static_cast<long long>(n);
+    a.m = static_cast<int>(m);
+    a.e = e;
+    a.width = width;
+    a.accept = d_accept_bitmap;
+    a.estimates = d_estimates;
+    a.outplanes = d_bits ? d.d_outplanes : nullptr;
+    a.err_flag = d.d_flag;
+    a.scratch = d.d_scratch;
+    a.scratch_words = d.scratch_words;
+    const bool short_circuit = e >= m;
+    const bool bad_width = width < 3 || width > 8;
+    if (short_circuit || bad_width)
+        PF_CUDA(sb::launch_validate(a, s));
+    else
+        PF_CUDA(sb::launch_filter(a, s));
+    uint32_t flag = 0;
+    PF_CUDA(cudaMemcpyAsync(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
+    PF_CUDA(cudaStreamSynchronize(s));
+    if (flag) {
+        const unsigned long long init = ~0ull;
+        PF_CUDA(cudaMemcpy(d.d_key, &init, sizeof(init), cudaMemcpyHostToDevice));
+        PF_CUDA(sb::launch_locate(d_text, d_pattern, pitch, a.n, a.m, d.d_key, s));
+        unsigned long long key = 0;
+        PF_CUDA(cudaMemcpyAsync(&key, d.d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+        PF_CUDA(cudaStreamSynchronize(s));
+        decode_illegal(key, 0, d_text, d_pattern, pitch, false, err);
+        return PF_ERR_ILLEGAL_CHARACTER;
+    }
+    if (bad_width) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS, "window width must be in [3, 8]");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    if (short_circuit)
+        PF_CUDA(sb::launch_accept_all(a.n, a.m, d_accept_bitmap, d_estimates, d_bits, s));
+    else if (d_bits)
+        PF_CUDA(sb::launch_bits_transpose(d.d_outplanes, a.n, a.m, d_bits, s));
+    return PF_OK;
+}
+
+int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                                  size_t pitch, size_t n, uint32_t m, uint32_t e, uint32_t width,
+                                  uint32_t* d_accept_bitmap, uint32_t* d_estimates,
+                                  uint32_t* d_err_flag, void* stream) {
+    pf_error* err = nullptr;
+    if (!ctx || !d_err_flag) return PF_ERR_NULL_ARGUMENT;
+    if (n == 0) return PF_OK;
+    if (!d_text || !d_pattern || !d_accept_bitmap) return PF_ERR_NULL_ARGUMENT;
+    if (m == 0) return PF_ERR_EMPTY_SEQUENCE;
+    if (e >= m || width < 3 || width > 8 || pitch % 16 != 0 || pitch < pf_device_pitch(m) ||
+        (reinterpret_cast<uintptr_t>(d_text) | reinterpret_cast<uintptr_t>(d_pattern)) % 16 != 0)
+        return PF_ERR_INVALID_PARAMETERS;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceState& d = ctx->devs[0];
+    PF_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    if (!sb::use_fused(width, e, static_cast<int>(m)))
+        PF_CUDA(grow(d.d_scratch, d.scratch_words,
+                     sb::generic_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
+    sb::FilterArgs a{};
+    a.text = d_text;
+    a.pattern = d_pattern;
+    a.pitch = pitch;
+    a.n = static_cast<long long>(n);
+    a.m = static_cast<int>(m);
+    a.e = e;
+    a.width = width;
+    a.accept = d_accept_bitmap;
+    a.estimates = d_estimates;
+    a.outplanes = nullptr;
+    a.err_flag = d_err_flag;
+    a.scratch = d.d_scratch;
+    a.scratch_words = d.scratch_words;
+    PF_CUDA(sb::launch_filter(a, s));
+    return PF_OK;
+}
+
+int pf_int_peak(pf_ctx* ctx, int op, double* ops_per_second) {
+    pf_error* err = nullptr;
+    if (!ctx || !ops_per_second) return PF_ERR_NULL_ARGUMENT;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceState& d = ctx->devs[0];
+    PF_CUDA(cudaSetDevice(d.device));
+    PF_CUDA(sb::measure_int_peak(op, d.stream, ops_per_second));
+    return PF_OK;
+}
+
+int pf_shouji_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, const char* text,
+                         size_t text_len, uint32_t e, uint32_t width, int* accept,
+                         uint32_t* estimate, uint64_t* bits, pf_error* err) {
+    if (err) std::memset(err, 0, sizeof(*err));
+    if (!ctx || !accept || !estimate) return PF_ERR_NULL_ARGUMENT;
+    if (pattern_len == 0 || text_len == 0) {
+        set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
+        return PF_ERR_EMPTY_SEQUENCE;
+    }
+    if (!pattern || !text) return PF_ERR_NULL_ARGUMENT;
+    // The caller's packed_sequence objects would have been built (and
+    // validated) before shouji_filter runs; pattern first, then text.
+    for (int field = 0; field < 2; ++field) {
+        const char* s = field == 0 ? pattern : text;
+        const size_t len = field == 0 ? pattern_len : text_len;
+        for (size_t i = 0; i < len; ++i) {
+            const char c = s[i];
+            if (c != 'A' && c != 'C' && c != 'G' && c != 'T' && c != 'N') {
+                if (err) {
+                    err->status = PF_ERR_ILLEGAL_CHARACTER;
+                    err->pair = 0;
+                    err->field = field == 0 ? 1u : 0u;  // 1 = pattern, 0 = text
+                    err->position = i;
+                    err->byte = static_cast<unsigned char>(c);
+                    std::snprintf(err->message, sizeof(err->message),
+                                  "illegal character at position %zu", i);
+                }
+                return PF_ERR_ILLEGAL_CHARACTER;
+            }
+        }
+    }
+    if (pattern_len != text_len) {  // shouji.cpp:44-45
+        set_err(err, PF_ERR_LENGTH_MISMATCH, "length mismatch");
+        return PF_ERR_LENGTH_MISMATCH;
+    }
+    if (width < 3 || width > 8) {  // shouji.cpp:47 (before the e >= m short-circuit)
+        set_err(err, PF_ERR_INVALID_PARAMETERS, "window width must be in [3, 8]");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    uint32_t acc = 0;
+    const int st = pf_shouji_filter_batch(ctx, reinterpret_cast<const uint8_t*>(text),
+                                          reinterpret_cast<const uint8_t*>(pattern), text_len, 1,
+                                          static_cast<uint32_t>(text_len), e, width, &acc, estimate,
+                                          bits, err);
+    if (st != PF_OK) return st;
+    *accept = static_cast<int>(acc & 1u);
+    return PF_OK;
+}
+
+void* pf_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void pf_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+int pf_generate_device(pf_ctx* ctx, int kind, uint64_t seed, uint32_t param, uint8_t* d_text,
+                       uint8_t* d_pattern, size_t pitch, size_t n, uint32_t m, void* stream) {
+    if (!ctx) return PF_ERR_NULL_ARGUMENT;
+    pf_error* err = nullptr;
+    DeviceState& d = ctx->devs[0];
+    PF_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    const cudaError_t st = sb::launch_generate(kind, seed, param, d_text, d_pattern, pitch,
+                                               static_cast<long long>(n), static_cast<int>(m), s);
+    if (st == cudaErrorInvalidValue) return PF_ERR_INVALID_PARAMETERS;
+    if (st != cudaSuccess) return PF_ERR_CUDA;
+    return PF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,316 @@
+// Fused width-4 Shouji kernel, specialised on the edit threshold E.
+//
+// Reference: shouji_filter (proj/src/shouji.cpp:41-58): build the 2E+1
+// diagonal mismatch vectors (neighborhood.cpp:41-79), then for j = 0..m-1
+// select_window (shouji.cpp:17-31) and commit_window (shouji.cpp:33-39), and
+// finally accept iff popcount(bv) <= E (shouji.cpp:56-57).
+//
+// One thread owns 32 consecutive pairs (pair-sliced words, see phase_a.cuh).
+// Per 16-column chunk the thread gathers the text chunk and a look-ahead
+// pattern chunk into a thread-private shared-memory ring (phase A), then runs
+// four blocks of four windows (phase B):
+//   * the diagonal loop d = -E..+E is fully unrolled and scanned in reference
+//     order; each new pattern column is one LDS per plane, kept in a sliding
+//     register window;
+//   * D_d for the block's columns is (Plo^Tlo)|(Phi^Thi)|PN|TN;
+//   * the window key is 2*ones + bit0 and the winner is the strict first
+//     minimum — exactly select_window's "more zeros, or equal zeros and a
+//     leading zero replacing a leading one" rule;
+//   * commit_window becomes a 3-bit state machine (fsm_step4): bit j+3 is
+//     always still 1 when window j is examined, so "strictly more zeros than
+//     the incumbent" is ones(best) <= popcount(bv[j..j+2]).
+//   * the final tally bits are summed in a bit-sliced counter; accept and the
+//     estimate fall out of it.
+// CARRY (E <= 12): the last three D columns of each diagonal are carried to
+// the next block in registers (3 new map words per window and diagonal).
+// Otherwise D is rebuilt over the block's 7 columns (fewer registers).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "bitslice.cuh"
+#include "kernels.cuh"
+#include "phase_a.cuh"
+
+namespace sb {
+
+struct Cand4 {
+    uint32_t k[4];  // key planes: k0 = slice bit 0, k1..k3 = ones count
+    uint32_t s[3];  // slice bits 1..3
+};
+
+__device__ __forceinline__ void make_cand4(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                           Cand4& out) {
+    const uint32_t s1 = a ^ b ^ c;
+    const uint32_t c1 = (a & b) | (a & c) | (b & c);
+    out.k[0] = a;
+    out.k[1] = s1 ^ d;
+    out.k[2] = c1 ^ (s1 & d);
+    out.k[3] = c1 & s1 & d;
+    out.s[0] = b;
+    out.s[1] = c;
+    out.s[2] = d;
+}
+
+__device__ __forceinline__ void update_best4(const Cand4& c, Cand4& best) {
+    const uint32_t lt = bs_less(c.k, best.k);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) best.k[i] = (c.k[i] & lt) | (best.k[i] & ~lt);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) best.s[i] = (c.s[i] & lt) | (best.s[i] & ~lt);
+}
+
+// commit_window as a state machine over S = tally bits (j, j+1, j+2).
+__device__ __forceinline__ uint32_t fsm_step4(const Cand4& best, uint32_t (&S)[3]) {
+    const uint32_t p0 = S[0] ^ S[1] ^ S[2];
+    const uint32_t p1 = (S[0] & S[1]) | (S[0] & S[2]) | (S[1] & S[2]);
+    const uint32_t x0 = ~best.k[1] | p0;
+    const uint32_t x1 = (~best.k[2] & p1) | (~(best.k[2] ^ p1) & x0);
+    const uint32_t commit = ~best.k[3] & x1;
+    const uint32_t out = (commit & best.k[0]) | (~commit & S[0]);
+    S[0] = (commit & best.s[0]) | (~commit & S[1]);
+    S[1] = (commit & best.s[1]) | (~commit & S[2]);
+    S[2] = best.s[2] | ~commit;
+    return out;
+}
+
+template <int E>
+struct FusedCfg {
+    static constexpr bool CARRY = E <= 12;
+    static constexpr int B = 4;                     // windows per block
+    static constexpr int LOOK = CARRY ? E : E + 3;  // pattern reach beyond the chunk
+    static constexpr int L = (LOOK + CH - 1) / CH;  // look-ahead chunks
+    static constexpr int R = 2 * L + 1;             // pattern ring slots
+    static constexpr int TR = CARRY ? 1 : 2;        // text ring slots
+    static constexpr int COLS = (TR + R) * CH;
+    static constexpr int BYTES_PER_THREAD = COLS * 3 * 4;
+    static constexpr int NT = BYTES_PER_THREAD * 128 <= 100 * 1024   ? 128
+                              : BYTES_PER_THREAD * 64 <= 100 * 1024 ? 64
+                                                                     : 32;
+    static constexpr size_t SMEM = size_t(BYTES_PER_THREAD) * NT;
+};
+
+template <int E>
+__global__ void __launch_bounds__(FusedCfg<E>::NT)
+shouji_fused_w4(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
+                size_t pitch, long long n, int m, uint32_t* __restrict__ accept,
+                uint32_t* __restrict__ estimates, uint32_t* __restrict__ outplanes,
+                uint32_t* __restrict__ err_flag) {
+    using Cfg = FusedCfg<E>;
+    constexpr int NT = Cfg::NT, L = Cfg::L, R = Cfg::R, TR = Cfg::TR, B = Cfg::B;
+    constexpr bool CARRY = Cfg::CARRY;
+    constexpr int NC = 8;  // counter planes: estimates up to 255 (m <= 255 here)
+    extern __shared__ uint32_t smem[];
+    const int tid = threadIdx.x;
+    const long long g = static_cast<long long>(blockIdx.x) * NT + tid;
+    const long long row0 = g * 32;
+    if (row0 >= n) return;
+    const long long ngroups = (n + 31) / 32;
+
+    uint32_t* const tring = smem + tid;                 // [TR*CH][3][NT]
+    uint32_t* const pring = smem + TR * CH * 3 * NT + tid;  // [R*CH][3][NT]
+    // Ring addressing: chunk q lives in slot q mod R (q >= -R*4 kept positive).
+    auto pcol = [&](int col) -> const uint32_t* {
+        const int q = (col + CH * R * 4) / CH;
+        return pring + (((q % R) * CH + (col & (CH - 1))) * 3) * NT;
+    };
+    auto tcol = [&](int col) -> const uint32_t* {
+        const int q = (col + CH * TR * 4) / CH;
+        return tring + (((q % TR) * CH + (col & (CH - 1))) * 3) * NT;
+    };
+
+    uint32_t err = 0u;
+    constexpr int DCN = CARRY ? 2 * E + 1 : 1;
+    uint32_t Dc[DCN][3];
+#pragma unroll
+    for (int di = 0; di < DCN; ++di) Dc[di][0] = Dc[di][1] = Dc[di][2] = ~0u;
+    uint32_t S[3] = {~0u, ~0u, ~0u};  // bitvector bv(m, true) (shouji.cpp:52)
+    uint32_t cnt[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) cnt[i] = 0u;
+
+    const int C = (m + 3 + CH - 1) / CH;  // chunks: windows must reach m-1
+    for (int t = -L; t < C; ++t) {
+        // ---- phase A: pattern chunk t+L, text chunk t (one inlined gather) --
+#pragma unroll 1
+        for (int sidx = 0; sidx < 2; ++sidx) {
+            const bool pat = sidx == 0;
+            const int q = pat ? t + L : t;
+            if (!pat && q < -(TR - 1)) break;
+            uint32_t* dst = pat ? pring + ((((q % R) + R) % R) * CH * 3) * NT
+                                : tring + ((((q % TR) + TR) % TR) * CH * 3) * NT;
+            err |= produce_chunk(pat ? pattern : text, pitch, row0, n, q, m, dst, NT);
+        }
+        if (t < 0) continue;
+        const int c = t;
+        // ---- phase B ---------------------------------------------------------
+#pragma unroll 1
+        for (int blk = 0; blk < CH / B; ++blk) {
+            const int j0 = c * CH - 3 + blk * B;  // first window of the block
+            Cand4 best[B];
+            if constexpr (CARRY) {
+                // new D columns j0+3 .. j0+3+B-1; pattern column = that + d
+                uint32_t T[B][3];
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const uint32_t* p = tcol(j0 + 3 + b);
+                    T[b][0] = p[0];
+                    T[b][1] = p[NT];
+                    T[b][2] = p[2 * NT];
+                }
+                uint32_t P[B][3];
+#pragma unroll
+                for (int di = 0; di <= 2 * E; ++di) {
+                    if (di == 0) {
+#pragma unroll
+                        for (int b = 0; b < B; ++b) {
+                            const uint32_t* p = pcol(j0 + 3 + b - E);
+                            P[b][0] = p[0];
+                            P[b][1] = p[NT];
+                            P[b][2] = p[2 * NT];
+                        }
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < B - 1; ++b) {
+                            P[b][0] = P[b + 1][0];
+                            P[b][1] = P[b + 1][1];
+                            P[b][2] = P[b + 1][2];
+                        }
+                        const uint32_t* p = pcol(j0 + 3 + B - 1 - E + di);
+                        P[B - 1][0] = p[0];
+                        P[B - 1][1] = p[NT];
+                        P[B - 1][2] = p[2 * NT];
+                    }
+                    uint32_t s[B + 3];
+                    s[0] = Dc[CARRY ? di : 0][0];
+                    s[1] = Dc[CARRY ? di : 0][1];
+                    s[2] = Dc[CARRY ? di : 0][2];
+#pragma unroll
+                    for (int b = 0; b < B; ++b)
+                        s[3 + b] = (P[b][0] ^ T[b][0]) | (P[b][1] ^ T[b][1]) | P[b][2] | T[b][2];
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        Cand4 cd;
+                        make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
+                        if (di == 0)
+                            best[b] = cd;
+                        else
+                            update_best4(cd, best[b]);
+                    }
+                    Dc[CARRY ? di : 0][0] = s[B];
+                    Dc[CARRY ? di : 0][1] = s[B + 1];
+                    Dc[CARRY ? di : 0][2] = s[B + 2];
+                }
+            } else {
+                // D over columns j0 .. j0+B+2 rebuilt per block.
+                constexpr int X = B + 3;
+                uint32_t T[X][3];
+#pragma unroll
+                for (int x = 0; x < X; ++x) {
+                    const uint32_t* p = tcol(j0 + x);
+                    T[x][0] = p[0];
+                    T[x][1] = p[NT];
+                    T[x][2] = p[2 * NT];
+                }
+                uint32_t P[X][3];
+#pragma unroll
+                for (int di = 0; di <= 2 * E; ++di) {
+                    if (di == 0) {
+#pragma unroll
+                        for (int x = 0; x < X; ++x) {
+                            const uint32_t* p = pcol(j0 + x - E);
+                            P[x][0] = p[0];
+                            P[x][1] = p[NT];
+                            P[x][2] = p[2 * NT];
+                        }
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < X - 1; ++x) {
+                            P[x][0] = P[x + 1][0];
+                            P[x][1] = P[x + 1][1];
+                            P[x][2] = P[x + 1][2];
+                        }
+                        const uint32_t* p = pcol(j0 + X - 1 - E + di);
+                        P[X - 1][0] = p[0];
+                        P[X - 1][1] = p[NT];
+                        P[X - 1][2] = p[2 * NT];
+                    }
+                    uint32_t s[X];
+#pragma unroll
+                    for (int x = 0; x < X; ++x)
+                        s[x] = (P[x][0] ^ T[x][0]) | (P[x][1] ^ T[x][1]) | P[x][2] | T[x][2];
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        Cand4 cd;
+                        make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
+                        if (di == 0)
+                            best[b] = cd;
+                        else
+                            update_best4(cd, best[b]);
+                    }
+                }
+            }
+            // commit chain over the block's windows, in column order
+            uint32_t outs[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const int j = j0 + b;
+                outs[b] = 0u;
+                if (j >= 0 && j < m) {
+                    outs[b] = fsm_step4(best[b], S);
+                    if (outplanes) outplanes[static_cast<long long>(j) * ngroups + g] = outs[b];
+                }
+            }
+            uint32_t v[3];
+            {
+                const uint32_t s1 = outs[0] ^ outs[1] ^ outs[2];
+                const uint32_t c1 = (outs[0] & outs[1]) | (outs[0] & outs[2]) | (outs[1] & outs[2]);
+                v[0] = s1 ^ outs[3];
+                v[1] = c1 ^ (s1 & outs[3]);
+                v[2] = c1 & s1 & outs[3];
+            }
+            bs_add(cnt, v);
+        }
+    }
+
+    // accept = ones <= e (shouji.cpp:56-57); bits of pairs past n are 0.
+    const long long valid = n - row0;
+    const uint32_t vmask = valid >= 32 ? ~0u : ((1u << valid) - 1u);
+    accept[g] = bs_le_const(cnt, static_cast<uint32_t>(E)) & vmask;
+    if (estimates) {
+#pragma unroll 1
+        for (int b = 0; b < 32 && b < valid; ++b) {
+            uint32_t est = 0;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) est |= ((cnt[i] >> b) & 1u) << i;
+            estimates[row0 + b] = est;
+        }
+    }
+    if (err) atomicOr(err_flag, 1u);
+}
+
+template <int E>
+cudaError_t launch_fused_e(const FilterArgs& a, cudaStream_t s) {
+    using Cfg = FusedCfg<E>;
+    auto kern = shouji_fused_w4<E>;
+    static bool attr_set = false;  // per instantiation; the call is idempotent
+    if (!attr_set) {
+        cudaError_t st = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(Cfg::SMEM));
+        if (st != cudaSuccess) return st;
+        attr_set = true;
+    }
+    const long long ngroups = (a.n + 31) / 32;
+    const unsigned grid = static_cast<unsigned>((ngroups + Cfg::NT - 1) / Cfg::NT);
+    kern<<<grid, Cfg::NT, Cfg::SMEM, s>>>(a.text, a.pattern, a.pitch, a.n, a.m, a.accept,
+                                          a.estimates, a.outplanes, a.err_flag);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace sb
+
+// Explicit instantiation helper for the fused_e*.cu units.
+#define SB_INSTANTIATE_FUSED(E) \
+    template cudaError_t sb::launch_fused_e<E>(const sb::FilterArgs&, cudaStream_t);

@@ -1,0 +1,348 @@
+// sm_100a kernels for the Shouji pre-alignment filter (arXiv 1809.07858).
+//
+// Reference hot path: prefilter::shouji_filter, proj/src/shouji.cpp:41-58,
+// with neighborhood_map (proj/src/neighborhood.cpp:41-79), select_window
+// (shouji.cpp:17-31), commit_window (shouji.cpp:33-39) and the codec
+// packed_sequence::from_string (proj/src/packed_sequence.cpp:7-34).
+//
+// Design (DESIGN.md has the long form): PAIR-SLICED bit logic. One thread
+// owns 32 consecutive pairs; every register word holds one bit of 32 pairs
+// (bit b = pair 32*group + b). Nothing is ever serial per pair: the
+// neighbourhood map, the window search, the commit step and the edit count
+// are all 32-pair-wide LOP3 expressions. The reference's serial commit chain
+// over columns becomes an 8-state machine (Appendix B2 of SURVEY.md) applied
+// to 32 pairs per instruction.
+//
+//   phase A  (gather_chunk): 16 ASCII columns x 32 pairs are loaded with
+//            128-bit loads and bit-transposed in registers (funnel-rotate +
+//            LOP3 gather, then a PRMT 4x4 byte transpose) into per-column
+//            plane words lo/hi/N (ASCII bits 1/2/3), validating every byte on
+//            the way. Planes go to a thread-private shared-memory ring.
+//   phase B  (search + commit): per block of 4 windows, the 2E+1 diagonals
+//            are scanned in reference order with the strict-first-argmax key
+//            2*ones + bit0 (equivalent to shouji.cpp:26-28);
+//            the chosen slices drive the commit FSM and a bit-sliced counter.
+//
+// Everything a thread touches in shared memory is private to it, so the
+// kernel has no barriers.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "bitslice.cuh"
+#include "kernels.cuh"
+#include "phase_a.cuh"
+
+#include <array>
+#include <utility>
+
+namespace sb {
+
+static std::atomic<uint64_t> g_launches{0};
+uint64_t launch_count() { return g_launches.load(); }
+void count_launch(int k) { g_launches.fetch_add(static_cast<uint64_t>(k)); }
+
+// ---------------------------------------------------------------------------
+// Generic path: any width 3..8, any e < m. Two kernels: pack (phase A into
+// global planes [col][3][ngroups]) and a plain pair-sliced sweep reading them.
+// ---------------------------------------------------------------------------
+constexpr int kPackNT = 128;
+
+__global__ void __launch_bounds__(kPackNT)
+pack_planes(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern, size_t pitch,
+            long long n, int m, uint32_t* __restrict__ tplanes, uint32_t* __restrict__ pplanes,
+            uint32_t* __restrict__ err_flag) {
+    const long long g = static_cast<long long>(blockIdx.x) * kPackNT + threadIdx.x;
+    const long long ngroups = (n + 31) / 32;
+    if (g >= ngroups) return;
+    const long long row0 = g * 32;
+    uint32_t err = 0u;
+    const int C = (m + CH - 1) / CH;
+    for (int c = 0; c < C; ++c) {
+        // columns >= m of the last chunk land in the scratch padding (C*CH columns)
+        err |= produce_chunk(text, pitch, row0, n, c, m, tplanes + (size_t(c) * CH * 3) * ngroups + g,
+                             static_cast<int>(ngroups));
+        err |= produce_chunk(pattern, pitch, row0, n, c, m,
+                             pplanes + (size_t(c) * CH * 3) * ngroups + g, static_cast<int>(ngroups));
+    }
+    if (err) atomicOr(err_flag, 1u);
+}
+
+template <int W>
+struct WCfg {
+    static constexpr int NO = W >= 8 ? 4 : (W >= 4 ? 3 : 2);  // planes for ones in [0, W]
+    static constexpr int NK = NO + 1;                          // key = 2*ones + bit0
+    static constexpr int NS = W - 1 >= 4 ? 3 : (W - 1 >= 2 ? 2 : 1);  // planes for popcount(S)
+};
+
+template <int W, int NC>
+__global__ void __launch_bounds__(128)
+shouji_generic(const uint32_t* __restrict__ tplanes, const uint32_t* __restrict__ pplanes,
+               long long n, int m, int e, uint32_t* __restrict__ accept,
+               uint32_t* __restrict__ estimates, uint32_t* __restrict__ outplanes) {
+    using Cfg = WCfg<W>;
+    const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long ngroups = (n + 31) / 32;
+    if (g >= ngroups) return;
+    const long long row0 = g * 32;
+    auto tp = [&](int col, int k) { return tplanes[(size_t(col) * 3 + k) * ngroups + g]; };
+    auto pp = [&](int col, int k) { return pplanes[(size_t(col) * 3 + k) * ngroups + g]; };
+
+    uint32_t S[W - 1];
+#pragma unroll
+    for (int i = 0; i < W - 1; ++i) S[i] = ~0u;
+    uint32_t cnt[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) cnt[i] = 0u;
+
+    for (int j = 0; j < m; ++j) {
+        uint32_t tw[W][3];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int col = j + k;
+            if (col < m) {
+                tw[k][0] = tp(col, 0);
+                tw[k][1] = tp(col, 1);
+                tw[k][2] = tp(col, 2);
+            } else {
+                tw[k][0] = tw[k][1] = 0u;
+                tw[k][2] = ~0u;
+            }
+        }
+        uint32_t bk[Cfg::NK], bsl[W];
+        for (int d = -e; d <= e; ++d) {
+            uint32_t sl[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const int pc = j + k + d;
+                uint32_t plo = 0u, phi = 0u, pn = ~0u;
+                if (pc >= 0 && pc < m) {
+                    plo = pp(pc, 0);
+                    phi = pp(pc, 1);
+                    pn = pp(pc, 2);
+                }
+                sl[k] = (plo ^ tw[k][0]) | (phi ^ tw[k][1]) | pn | tw[k][2];
+            }
+            uint32_t ones[Cfg::NO];
+            bs_popcount<W>(sl, ones);
+            uint32_t key[Cfg::NK];
+            key[0] = sl[0];
+#pragma unroll
+            for (int i = 0; i < Cfg::NO; ++i) key[i + 1] = ones[i];
+            if (d == -e) {
+#pragma unroll
+                for (int i = 0; i < Cfg::NK; ++i) bk[i] = key[i];
+#pragma unroll
+                for (int k = 0; k < W; ++k) bsl[k] = sl[k];
+            } else {
+                const uint32_t lt = bs_less(key, bk);
+#pragma unroll
+                for (int i = 0; i < Cfg::NK; ++i) bk[i] = (key[i] & lt) | (bk[i] & ~lt);
+#pragma unroll
+                for (int k = 0; k < W; ++k) bsl[k] = (sl[k] & lt) | (bsl[k] & ~lt);
+            }
+        }
+        // commit: ones(best) <= popcount(S)  (general form of fsm_step4)
+        uint32_t ps[Cfg::NS];
+        bs_popcount<W - 1>(S, ps);
+        uint32_t ones[Cfg::NO];
+#pragma unroll
+        for (int i = 0; i < Cfg::NO; ++i) ones[i] = bk[i + 1];
+        const uint32_t commit = ~bs_less(ps, ones);
+        const uint32_t out = (commit & bsl[0]) | (~commit & S[0]);
+#pragma unroll
+        for (int i = 0; i < W - 2; ++i) S[i] = (commit & bsl[i + 1]) | (~commit & S[i + 1]);
+        S[W - 2] = bsl[W - 1] | ~commit;
+        if (outplanes) outplanes[static_cast<long long>(j) * ngroups + g] = out;
+        const uint32_t one[1] = {out};
+        bs_add(cnt, one);
+    }
+    const long long valid = n - row0;
+    const uint32_t vmask = valid >= 32 ? ~0u : ((1u << valid) - 1u);
+    accept[g] = bs_le_const(cnt, static_cast<uint32_t>(e)) & vmask;
+    if (estimates) {
+        for (int b = 0; b < 32 && b < valid; ++b) {
+            uint32_t est = 0;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) est |= ((cnt[i] >> b) & 1u) << i;
+            estimates[row0 + b] = est;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Error location, tally transpose, short-circuit fill.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool valid_base(uint8_t c) {
+    return c == 'A' || c == 'C' || c == 'G' || c == 'T' || c == 'N';
+}
+
+__global__ void locate_illegal(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
+                               size_t pitch, long long n, int m, unsigned long long* key) {
+    const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    for (int field = 0; field < 2; ++field) {
+        const uint8_t* s = (field == 0 ? text : pattern) + p * pitch;
+        for (int i = 0; i < m; ++i) {
+            if (!valid_base(s[i])) {
+                const unsigned long long k =
+                    (static_cast<unsigned long long>(p * 2 + field) << 24) | static_cast<unsigned>(i);
+                atomicMin(key, k);
+                return;
+            }
+        }
+    }
+}
+
+__global__ void bits_transpose(const uint32_t* __restrict__ outplanes, long long n, int m,
+                               uint64_t* __restrict__ bits) {
+    const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const long long ngroups = (n + 31) / 32;
+    const long long g = p / 32;
+    const int b = static_cast<int>(p % 32);
+    const int words = (m + 63) / 64;
+    for (int w = 0; w < words; ++w) {
+        uint64_t v = 0;
+        for (int t = 0; t < 64; ++t) {
+            const int j = 64 * w + t;
+            if (j >= m) break;
+            v |= static_cast<uint64_t>((outplanes[static_cast<long long>(j) * ngroups + g] >> b) & 1u) << t;
+        }
+        bits[p * words + w] = v;
+    }
+}
+
+__global__ void accept_all(long long n, int m, uint32_t* accept, uint32_t* estimates, uint64_t* bits) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long ngroups = (n + 31) / 32;
+    if (i < ngroups) {
+        const long long valid = n - i * 32;
+        accept[i] = valid >= 32 ? ~0u : ((1u << valid) - 1u);
+    }
+    if (i < n) {
+        if (estimates) estimates[i] = 0u;
+        if (bits) {
+            const int words = (m + 63) / 64;
+            for (int w = 0; w < words; ++w) bits[i * words + w] = 0ull;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers.
+// ---------------------------------------------------------------------------
+// Defined in fused.cuh, explicitly instantiated in fused_e*.cu (compiled in
+// parallel: each E is its own fully unrolled kernel).
+template <int E>
+cudaError_t launch_fused_e(const FilterArgs& a, cudaStream_t s);
+
+using FusedFn = cudaError_t (*)(const FilterArgs&, cudaStream_t);
+template <int... Es>
+static constexpr std::array<FusedFn, sizeof...(Es)> make_fused_table(std::integer_sequence<int, Es...>) {
+    return {&launch_fused_e<Es>...};
+}
+static constexpr auto kFusedTable = make_fused_table(std::make_integer_sequence<int, kFusedMaxE + 1>{});
+
+template <int W, int NC>
+static cudaError_t launch_generic_w(const FilterArgs& a, cudaStream_t s) {
+    const long long ngroups = (a.n + 31) / 32;
+    const int C = (a.m + CH - 1) / CH;
+    uint32_t* tpl = a.scratch;
+    uint32_t* ppl = a.scratch + size_t(C) * CH * 3 * ngroups;
+    const unsigned gp = static_cast<unsigned>((ngroups + kPackNT - 1) / kPackNT);
+    pack_planes<<<gp, kPackNT, 0, s>>>(a.text, a.pattern, a.pitch, a.n, a.m, tpl, ppl, a.err_flag);
+    count_launch();
+    cudaError_t st = cudaGetLastError();
+    if (st != cudaSuccess) return st;
+    shouji_generic<W, NC><<<gp, 128, 0, s>>>(tpl, ppl, a.n, a.m, static_cast<int>(a.e), a.accept,
+                                             a.estimates, a.outplanes);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <int NC>
+static cudaError_t launch_generic(const FilterArgs& a, cudaStream_t s) {
+    switch (a.width) {
+        case 3: return launch_generic_w<3, NC>(a, s);
+        case 4: return launch_generic_w<4, NC>(a, s);
+        case 5: return launch_generic_w<5, NC>(a, s);
+        case 6: return launch_generic_w<6, NC>(a, s);
+        case 7: return launch_generic_w<7, NC>(a, s);
+        case 8: return launch_generic_w<8, NC>(a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+size_t generic_scratch_words(long long n, int m) {
+    const long long ngroups = (n + 31) / 32;
+    const long long C = (m + CH - 1) / CH;
+    return static_cast<size_t>(2 * C * CH * 3 * ngroups);
+}
+
+bool use_fused(uint32_t width, uint32_t e, int m) {
+    return width == 4 && e <= static_cast<uint32_t>(kFusedMaxE) && m <= 255;
+}
+
+cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
+    if (a.n <= 0) return cudaSuccess;
+    const bool small = a.m <= 255;
+    if (use_fused(a.width, a.e, a.m)) return kFusedTable[a.e](a, s);
+    if (a.scratch == nullptr || a.scratch_words < generic_scratch_words(a.n, a.m))
+        return cudaErrorInvalidValue;
+    return small ? launch_generic<8>(a, s) : launch_generic<24>(a, s);
+}
+
+__global__ void __launch_bounds__(kPackNT)
+validate_only(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern, size_t pitch,
+              long long n, int m, uint32_t* __restrict__ err_flag) {
+    __shared__ uint32_t sink[CH * 3 * kPackNT];
+    const long long g = static_cast<long long>(blockIdx.x) * kPackNT + threadIdx.x;
+    const long long ngroups = (n + 31) / 32;
+    if (g >= ngroups) return;
+    const long long row0 = g * 32;
+    uint32_t err = 0u;
+    const int C = (m + CH - 1) / CH;
+    for (int c = 0; c < C; ++c) {
+        err |= produce_chunk(text, pitch, row0, n, c, m, sink + threadIdx.x, kPackNT);
+        err |= produce_chunk(pattern, pitch, row0, n, c, m, sink + threadIdx.x, kPackNT);
+    }
+    if (err) atomicOr(err_flag, 1u);
+}
+
+cudaError_t launch_validate(const FilterArgs& a, cudaStream_t s) {
+    if (a.n <= 0) return cudaSuccess;
+    const long long ngroups = (a.n + 31) / 32;
+    const unsigned gp = static_cast<unsigned>((ngroups + kPackNT - 1) / kPackNT);
+    validate_only<<<gp, kPackNT, 0, s>>>(a.text, a.pattern, a.pitch, a.n, a.m, a.err_flag);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_locate(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
+                          int m, unsigned long long* d_key, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>((n + 127) / 128);
+    locate_illegal<<<grid, 128, 0, s>>>(text, pattern, pitch, n, m, d_key);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bits_transpose(const uint32_t* outplanes, long long n, int m, uint64_t* bits,
+                                  cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>((n + 127) / 128);
+    bits_transpose<<<grid, 128, 0, s>>>(outplanes, n, m, bits);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_accept_all(long long n, int m, uint32_t* accept, uint32_t* estimates,
+                              uint64_t* bits, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned grid = static_cast<unsigned>((n + 127) / 128);
+    accept_all<<<grid, 128, 0, s>>>(n, m, accept, estimates, bits);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace sb

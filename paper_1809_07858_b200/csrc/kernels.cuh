@@ -1,0 +1,57 @@
+// Internal launch interface between the C ABI (capi.cpp) and the sm_100a
+// kernels (kernels.cu). Not installed; not part of the public boundary.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace sb {
+
+// Largest E served by the fused, E-specialised width-4 kernel; larger E and
+// widths other than 4 run the two-kernel generic path.
+constexpr int kFusedMaxE = 31;
+
+struct FilterArgs {
+    const uint8_t* text;     // device, [n][pitch]
+    const uint8_t* pattern;  // device, [n][pitch]
+    size_t pitch;
+    long long n;
+    int m;
+    uint32_t e;
+    uint32_t width;
+    uint32_t* accept;      // device, ceil(n/32) words
+    uint32_t* estimates;   // device, n, may be null
+    uint32_t* outplanes;   // device scratch [m][ngroups] or null (tally dump)
+    uint32_t* err_flag;    // device, 1 word, zeroed by the caller
+    uint32_t* scratch;     // device scratch for the generic path (planes)
+    size_t scratch_words;  // available words in scratch
+};
+
+size_t generic_scratch_words(long long n, int m);
+bool use_fused(uint32_t width, uint32_t e, int m);
+
+// Launch the filter (fused or generic). Returns a cudaError_t.
+cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s);
+// Validation only (for e >= m or an invalid width): sets *err_flag on any illegal byte.
+cudaError_t launch_validate(const FilterArgs& a, cudaStream_t s);
+// First illegal byte: key = ((pair*2+field) << 24) | pos into *d_key (pre-set to ~0).
+cudaError_t launch_locate(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
+                          int m, unsigned long long* d_key, cudaStream_t s);
+// [m][ngroups] tally plane words -> per-pair bitvector words.
+cudaError_t launch_bits_transpose(const uint32_t* outplanes, long long n, int m, uint64_t* bits,
+                                  cudaStream_t s);
+// e >= m short-circuit outputs.
+cudaError_t launch_accept_all(long long n, int m, uint32_t* accept, uint32_t* estimates,
+                              uint64_t* bits, cudaStream_t s);
+cudaError_t launch_generate(int kind, uint64_t seed, uint32_t param, uint8_t* text,
+                            uint8_t* pattern, size_t pitch, long long n, int m, cudaStream_t s);
+
+// Integer pipe microbenchmark (diagnostic): lane-ops per second for op
+// 0 LOP3, 1 SHF (funnel), 2 PRMT, 3 IMAD.
+cudaError_t measure_int_peak(int op, cudaStream_t s, double* ops_per_second);
+
+uint64_t launch_count();
+void count_launch(int k = 1);
+
+}  // namespace sb

@@ -1,0 +1,158 @@
+// Phase A of the pair-sliced Shouji kernels: ASCII records -> bit planes.
+//
+// Reference: packed_sequence::from_string (proj/src/packed_sequence.cpp:7-34)
+// packs A/C/G/T into two code planes plus an N plane and throws on any other
+// byte. Here one thread converts a 16-column x 32-pair tile of one sequence
+// into 16 column words per plane, where bit b of a column word belongs to
+// pair row0+b ("pair-sliced" layout).
+//
+// Encoding: ASCII bits 1/2/3 of A,C,G,T,N are (lo,hi,N) = 000,100,110,010,111.
+// A,C,G,T get distinct (bit1,bit2) codes and only N sets bit 3, so
+//   mismatch = (Plo^Tlo) | (Phi^Thi) | PN | TN
+// is exactly !bases_match (packed_sequence.hpp:58-61; N matches nothing,
+// itself included). Columns outside [0, m) are forced to N: that realises both
+// boundary rules of the reference — a pattern index outside [0,m) is a
+// mismatch (neighborhood.cpp:71-76) and window reads past the text read as 1
+// (bitvector.hpp:88-91) — with no special cases in phase B.
+//
+// Validation is exact and costs no extra pass: a byte is in {A,C,G,T,N} iff
+// bits 7..5 are 010 (raw OR/AND accumulators over the loaded words) and,
+// given (b3,b2,b1) in {000,001,011,010,111}, b0 == ~b3&(~b2|b1) and
+// b4 == b2&~b1&~b3 (checked on the gathered planes). Any failure only raises a
+// flag; the host then runs a locator kernel for the reference's exact error
+// (lowest pair, text before pattern, lowest position).
+#pragma once
+#include <cstdint>
+
+#include "bitslice.cuh"
+
+namespace sb {
+
+constexpr int CH = 16;  // columns per chunk (one 128-bit load per row)
+
+// Compile-time rotate for mask constants (s may be negative).
+__host__ __device__ constexpr uint32_t crotl(uint32_t x, int s) {
+    return ((s % 32) + 32) % 32 == 0
+               ? x
+               : (x << (((s % 32) + 32) % 32)) | (x >> (32 - ((s % 32) + 32) % 32));
+}
+
+// Gather columns [col0, col0+16) of rows [row0, row0+32) into plane words.
+// dst[(col*3 + k) * dstride], k = 0 lo, 1 hi, 2 N. Returns nonzero on any
+// illegal byte. EDGE: the chunk straddles m (bytes at columns >= m are
+// ignored and their planes forced to N).
+template <bool EDGE>
+__device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq, size_t pitch,
+                                                 long long row0, long long n, int col0, int m,
+                                                 uint32_t* __restrict__ dst, int dstride) {
+    uint32_t O[4][3][4];  // [column group][plane][column in group] -> column words
+#pragma unroll
+    for (int cg = 0; cg < 4; ++cg)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) O[cg][k][q] = 0u;
+    uint32_t orr = 0u, andd = ~0u, err = 0u;
+    uint32_t cm[4];
+    if (EDGE) {
+#pragma unroll
+        for (int cg = 0; cg < 4; ++cg) {
+            uint32_t mask = 0u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (col0 + 4 * cg + q < m) mask |= 0xFFu << (8 * q);
+            cm[cg] = mask;
+        }
+    }
+    // Rows are consumed in groups of 8 (one byte lane of 8 pairs per column);
+    // the loop stays rolled so at most 8 row loads are in flight per thread.
+#pragma unroll 1
+    for (int g8 = 0; g8 < 4; ++g8) {
+        uint4 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const long long row = row0 + 8 * g8 + i;
+            if (row < n)
+                v[i] = __ldg(reinterpret_cast<const uint4*>(seq + row * pitch + col0));
+            else
+                v[i] = make_uint4(0x41414141u, 0x41414141u, 0x41414141u, 0x41414141u);
+        }
+        uint32_t acc[5][4];
+#pragma unroll
+        for (int k = 0; k < 5; ++k)
+#pragma unroll
+            for (int cg = 0; cg < 4; ++cg) acc[k][cg] = 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t wv[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+            for (int cg = 0; cg < 4; ++cg) {
+                uint32_t w = wv[cg];
+                if (EDGE) w = (w & cm[cg]) | (0x41414141u & ~cm[cg]);
+                orr |= w;
+                andd &= w;
+                // bit (8q+k) of w lands at (8q+k+i-1) mod 32 for every byte q
+                const uint32_t u = rotl(w, i - 1);
+#pragma unroll
+                for (int k = 0; k < 5; ++k) acc[k][cg] |= u & crotl(0x01010101u, k + i - 1);
+            }
+        }
+#pragma unroll
+        for (int cg = 0; cg < 4; ++cg) {
+            // undo the per-plane offset: bit (8q+i) = bit k of (row 8*g8+i, column 4cg+q)
+            const uint32_t p0 = rotl(acc[0][cg], 1);
+            const uint32_t p1 = acc[1][cg];
+            const uint32_t p2 = rotr(acc[2][cg], 1);
+            const uint32_t p3 = rotr(acc[3][cg], 2);
+            const uint32_t p4 = rotr(acc[4][cg], 3);
+            const uint32_t g0 = ~p3 & (~p2 | p1);
+            const uint32_t gg4 = p2 & ~p1 & ~p3;
+            err |= (p0 ^ g0) | (p4 ^ gg4) | (p3 & ~(p2 & p1));
+            const uint32_t P[3] = {p1, p2, p3};
+            // byte q of P (column 4cg+q, pairs 8g8..8g8+7) becomes byte g8 of the
+            // column word: shift the word down one byte and insert at the top.
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    O[cg][k][q] = __byte_perm(O[cg][k][q], P[k], 0x0321 | ((4 + q) << 12));
+        }
+    }
+    err |= (orr & 0xA0A0A0A0u) | (~andd & 0x40404040u);
+#pragma unroll
+    for (int cg = 0; cg < 4; ++cg)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int col = 4 * cg + q;
+                uint32_t val = O[cg][k][q];
+                if (EDGE && k == 2 && col0 + col >= m) val = ~0u;
+                dst[(col * 3 + k) * dstride] = val;
+            }
+    return err;
+}
+
+// A chunk entirely outside [0, m): every column is N.
+__device__ __forceinline__ void fill_oob_chunk(uint32_t* __restrict__ dst, int dstride) {
+#pragma unroll
+    for (int col = 0; col < CH; ++col) {
+        dst[(col * 3 + 0) * dstride] = 0u;
+        dst[(col * 3 + 1) * dstride] = 0u;
+        dst[(col * 3 + 2) * dstride] = ~0u;
+    }
+}
+
+__device__ __forceinline__ uint32_t produce_chunk(const uint8_t* __restrict__ seq, size_t pitch,
+                                                  long long row0, long long n, int chunk, int m,
+                                                  uint32_t* __restrict__ dst, int dstride) {
+    const int col0 = chunk * CH;
+    if (chunk < 0 || col0 >= m) {
+        fill_oob_chunk(dst, dstride);
+        return 0u;
+    }
+    if (col0 + CH <= m) return gather_chunk<false>(seq, pitch, row0, n, col0, m, dst, dstride);
+    return gather_chunk<true>(seq, pitch, row0, n, col0, m, dst, dstride);
+}
+
+}  // namespace sb

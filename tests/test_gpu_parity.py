@@ -1,0 +1,335 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bar: bit-exact accept bitmaps AND edit estimates (and tally bits where the
+reference exposes them) on the same bytes. Sizes here are what the oracle
+finishes in seconds; full BASELINE sizes are covered by size-independent
+properties in test_gpu_fullsize.py.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+GOLDEN_TEXT = "GGTGCAGAGCTC"
+GOLDEN_PATTERN = "GGTGAGAGTTGT"
+
+
+def bitmap_bools(acc, n):
+    return np.unpackbits(np.ascontiguousarray(acc, np.uint32).view(np.uint8), bitorder="little")[:n].astype(bool)
+
+
+def check_batch(gpu, oracle, t, p, e, width=4, bits=False, **kw):
+    a1, e1, b1 = gpu.shouji_filter_batch(t, p, e, width, estimates=True, bits=bits, **kw)
+    a2, e2, b2 = oracle.shouji_batch(t, p, e, width, bits=bits)
+    n = t.shape[0]
+    bad = np.nonzero(bitmap_bools(a1, n) != bitmap_bools(a2, n))[0]
+    assert bad.size == 0, f"accept differs at pairs {bad[:10]} (m={t.shape[1]} e={e} w={width})"
+    bad = np.nonzero(e1 != e2)[0]
+    assert bad.size == 0, f"estimate differs at {bad[:10]}: gpu {e1[bad[:5]]} oracle {e2[bad[:5]]}"
+    assert (a1 == a2).all()
+    if bits:
+        assert (b1 == b2).all()
+    return a1, e1
+
+
+# --- the reference's unit tests (proj/tests/test_shouji.cpp) through our API ------
+
+def test_golden_pair(gpu):
+    d = gpu.shouji_filter(gpu.seq(GOLDEN_PATTERN), gpu.seq(GOLDEN_TEXT), 3)
+    assert d.accept and d.edit_estimate == 3
+    assert d.bits.to_string() == "000010000101" and d.bits.count_zeros() == 9
+    d2 = gpu.shouji_filter(gpu.seq(GOLDEN_PATTERN), gpu.seq(GOLDEN_TEXT), 2)
+    assert not d2.accept and d2.edit_estimate > 2
+
+
+def test_identical_pairs_pass(gpu):
+    rng = np.random.default_rng(29)
+    for _ in range(30):
+        s = "".join(rng.choice(list("ACGT"), int(1 + rng.integers(0, 120))))
+        e = int(rng.integers(0, 6))
+        d = gpu.shouji_filter(gpu.seq(s), gpu.seq(s), e)
+        assert d.accept and d.edit_estimate == 0
+
+
+def test_accept_agrees_with_estimate(gpu):
+    rng = np.random.default_rng(37)
+    for _ in range(100):
+        m = int(1 + rng.integers(0, 100))
+        e = int(rng.integers(0, m + 2))
+        a = "".join(rng.choice(list("ACGT"), m))
+        b = "".join(rng.choice(list("ACGT"), m))
+        d = gpu.shouji_filter(gpu.seq(b), gpu.seq(a), e)
+        assert d.accept == (d.edit_estimate <= e)
+        assert d.bits.size() == m and d.edit_estimate == d.bits.count_ones()
+
+
+def test_compensating_indels(gpu):
+    text = ("CACCATCCCAGAGCCACACGGTGCCGCAGTCGTAGTCAACGCGGACGTGTGCTATATAGTAACGTGAC"
+            "AAATCAGGTTCACTGCGCTCTGCGCCATCGAT")
+    pattern = ("CACCATCCCAGAGCCACACGGTCGCCGCAGTCGTAGTCAACGCGGACGTGTGTATATAGTAACGTGAC"
+               "AAATCAGGTTCACTGCGCTCTGCGCCATCGAT")
+    d = gpu.shouji_filter(gpu.seq(pattern), gpu.seq(text), 2)
+    assert not d.accept and d.edit_estimate == 3
+    assert gpu.shouji_filter(gpu.seq(pattern), gpu.seq(text), 3).accept
+
+
+def test_oversized_threshold_and_validation(gpu):
+    d = gpu.shouji_filter(gpu.seq("ACGT"), gpu.seq("TGCA"), 4)
+    assert d.accept and d.edit_estimate == 0 and d.bits.count_ones() == 0
+    with pytest.raises(gpu.length_mismatch_error):
+        gpu.shouji_filter(gpu.seq("ACGT"), gpu.seq("ACG"), 1)
+    for w in (2, 9):
+        with pytest.raises(gpu.invalid_parameters_error):
+            gpu.shouji_filter(gpu.seq("ACGT"), gpu.seq("ACGT"), 1, w)
+    with pytest.raises(gpu.invalid_parameters_error):
+        gpu.shouji_filter(gpu.seq("ACGT"), gpu.seq("ACGT"), 99, 9)
+
+
+def test_hamming_at_threshold_zero(gpu, oracle):
+    rng = np.random.default_rng(31)
+    n, m = 4096, 50
+    a = np.frombuffer(b"ACGTN", np.uint8)[rng.integers(0, 5, size=(n, m))]
+    b = a.copy()
+    mask = rng.random(a.shape) < 0.2
+    b[mask] = np.frombuffer(b"ACGTN", np.uint8)[rng.integers(0, 5, size=int(mask.sum()))]
+    acc, est, _ = gpu.shouji_filter_batch(a, b, 0, estimates=True)
+    ham = ((a != b) | (a == ord("N")) | (b == ord("N"))).sum(1)
+    assert (est == ham).all()
+    assert (bitmap_bools(acc, n) == (ham == 0)).all()
+
+
+# --- fixtures from the reference library ------------------------------------------
+
+def test_edge_fixtures(gpu):
+    z = np.load(os.path.join(GOLD, "edge_cases.npz"))
+    keys = sorted({k.rsplit("_", 1)[0] for k in z.files})
+    for k in keys:
+        m, width, e = (int(x) for x in z[f"{k}_meta"])
+        acc, est, bits = gpu.shouji_filter_batch(z[f"{k}_text"], z[f"{k}_pattern"], e, width,
+                                                 estimates=True, bits=True)
+        assert (acc == z[f"{k}_accept"]).all(), (k, m, width, e)
+        assert (est == z[f"{k}_est"]).all(), (k, m, width, e)
+        assert (bits == z[f"{k}_bits"]).all(), (k, m, width, e)
+
+
+def test_config0_full(gpu, oracle):
+    # BASELINE.json configs[0]: generate_pairs({1809078580, 1M, 100, {0,10}}), E = 5.
+    import hashlib
+    z = np.load(os.path.join(GOLD, "config0.npz"))
+    t, p = oracle.generate_pairs(1809078580, 1_000_000, 100, 0, 10)
+    assert (t[:4096] == z["text_head"]).all()
+    acc, est, _ = gpu.shouji_filter_batch(t, p, 5, estimates=True)
+    assert hashlib.sha256(acc.tobytes()).digest() == z["accept_sha256"].tobytes()
+    assert int(est.astype(np.int64).sum()) == int(z["est_sum"])
+    assert (np.bincount(est, minlength=101) == z["est_hist"]).all()
+    _, est2, _ = oracle.shouji_batch(t, p, 5)
+    assert (est == est2).all()
+
+
+@pytest.mark.parametrize("m,e,lost", [(100, 2, 583), (100, 5, 41), (150, 7, 7), (250, 15, 0)])
+def test_acceptance_criterion2(gpu, oracle, m, e, lost):
+    z = np.load(os.path.join(GOLD, f"fr_m{m}_e{e}.npz"))
+    t, p = oracle.generate_pairs(int(z["seed"]), 100_000, m, 0, e)
+    acc, est, _ = gpu.shouji_filter_batch(t, p, e, estimates=True)
+    assert (acc == z["accept"]).all() and (est == z["est"]).all()
+    assert int((z["similar"] & ~bitmap_bools(acc, 100_000)).sum()) == lost
+
+
+# --- sweeps over E, widths, lengths -------------------------------------------------
+
+@pytest.mark.parametrize("e", list(range(0, 32)))
+def test_every_fused_threshold(gpu, oracle, e):
+    rng = np.random.default_rng(1000 + e)
+    m = 100 if e < 20 else 250
+    n = 3000
+    t = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=(n, m))]
+    p = t.copy()
+    mask = rng.random(p.shape) < 0.06
+    p[mask] = np.frombuffer(b"ACGTN", np.uint8)[rng.integers(0, 5, size=int(mask.sum()))]
+    for i in range(0, n, 3):  # frame shifts
+        s = int(rng.integers(1, 4))
+        p[i, 40:] = np.roll(p[i, 40:], s)
+    check_batch(gpu, oracle, t, p, e, bits=(e % 7 == 0))
+
+
+@pytest.mark.parametrize("width", [3, 4, 5, 6, 7, 8])
+def test_generic_widths(gpu, oracle, width):
+    rng = np.random.default_rng(width)
+    for m, e in [(100, 5), (37, 3), (150, 12), (64, 40)]:
+        t = np.frombuffer(b"ACGTN", np.uint8)[rng.integers(0, 5, size=(700, m))]
+        p = t.copy()
+        mask = rng.random(p.shape) < 0.1
+        p[mask] = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=int(mask.sum()))]
+        check_batch(gpu, oracle, t, p, e, width, bits=True)
+
+
+def test_large_threshold_generic_path(gpu, oracle):
+    rng = np.random.default_rng(5)
+    for m, e in [(200, 150), (100, 32), (250, 60), (300, 20), (600, 10)]:
+        t = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=(200, m))]
+        p = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=(200, m))]
+        check_batch(gpu, oracle, t, p, e)
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 4095, 4096, 4097, 70001])
+def test_ragged_pair_counts(gpu, oracle, n):
+    rng = np.random.default_rng(n)
+    m = 100
+    t = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=(n, m))]
+    p = t.copy()
+    mask = rng.random(p.shape) < 0.05
+    p[mask] = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=int(mask.sum()))]
+    a, _ = check_batch(gpu, oracle, t, p, 5)
+    if n % 32:
+        assert int(a[-1]) >> (n % 32) == 0  # bits past n are zero
+
+
+def test_lengths_and_strides(gpu, oracle):
+    rng = np.random.default_rng(77)
+    for m in [1, 2, 3, 4, 5, 15, 16, 17, 31, 32, 33, 63, 64, 65, 99, 128, 200, 255]:
+        stride = m + int(rng.integers(0, 9))
+        t = np.full((500, stride), ord("x"), np.uint8)  # bytes past m are ignored
+        p = np.full((500, stride), ord("y"), np.uint8)
+        t[:, :m] = np.frombuffer(b"ACGTN", np.uint8)[rng.integers(0, 5, size=(500, m))]
+        p[:, :m] = t[:, :m]
+        mask = rng.random((500, m)) < 0.15
+        p[:, :m][mask] = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=int(mask.sum()))]
+        for e in sorted({0, 1, 3, min(m, 6), m}):
+            a1, e1, b1 = gpu.shouji_filter_batch(t, p, e, m=m, estimates=True, bits=True)
+            a2, e2, b2 = oracle.shouji_batch(t[:, :m], p[:, :m], e, bits=True)
+            assert (a1 == a2).all() and (e1 == e2).all() and (b1 == b2).all(), (m, e)
+
+
+def test_low_complexity_and_n(gpu, oracle):
+    rng = np.random.default_rng(123)
+    n, m = 5000, 250
+    t = np.zeros((n, m), np.uint8)
+    for i in range(n):
+        per = int(rng.integers(1, 7))
+        unit = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=per)]
+        t[i] = np.resize(unit, m)
+    p = t.copy()
+    for i in range(n):
+        for _ in range(int(rng.integers(0, 12))):
+            pos = int(rng.integers(0, m))
+            p[i, pos:] = np.roll(p[i, pos:], int(rng.integers(-2, 3)))
+    nm = rng.random(p.shape) < 0.01
+    p[nm] = ord("N")
+    t[rng.random(t.shape) < 0.01] = ord("N")
+    for e in (0, 5, 15, 25):
+        check_batch(gpu, oracle, t, p, e)
+
+
+# --- device-generated BASELINE configs 1-4 (sampled) vs the oracle ------------------
+
+@pytest.mark.parametrize("kind,m,es", [(1, 100, [0, 2, 5, 10]), (2, 150, [0, 3, 7, 15]),
+                                       (3, 250, [0, 5, 25]), (4, 250, [25])])
+def test_device_configs(gpu, oracle, kind, m, es):
+    import torch
+    n = 20000 if m <= 150 else 6000
+    pitch = gpu.device_pitch(m)
+    for e in es:
+        tt = torch.empty((n, pitch), dtype=torch.uint8, device="cuda")
+        pt = torch.empty((n, pitch), dtype=torch.uint8, device="cuda")
+        gpu.generate_device(kind, 1809078580 + kind + 1000 * e, e, tt.data_ptr(), pt.data_ptr(),
+                            pitch, n, m)
+        torch.cuda.synchronize()
+        t = tt.cpu().numpy()[:, :m].copy()
+        p = pt.cpu().numpy()[:, :m].copy()
+        assert set(np.unique(t)).issubset(set(b"ACGTN"))
+        check_batch(gpu, oracle, t, p, e)
+        # device-resident entry point gives the same bitmap
+        acc = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+        est = torch.zeros(n, dtype=torch.int32, device="cuda")
+        gpu.shouji_filter_device(tt.data_ptr(), pt.data_ptr(), pitch, n, m, e, acc.data_ptr(),
+                                 d_estimates=est.data_ptr())
+        torch.cuda.synchronize()
+        a2, e2, _ = oracle.shouji_batch(t, p, e)
+        assert (acc.cpu().numpy().view(np.uint32) == a2).all()
+        assert (est.cpu().numpy().view(np.uint32) == e2).all()
+
+
+# --- errors --------------------------------------------------------------------------
+
+def test_illegal_characters(gpu):
+    rng = np.random.default_rng(9)
+    n, m = 5000, 100
+    t = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=(n, m))].copy()
+    p = t.copy()
+    p[3000, 17] = ord("a")       # lower case is illegal (packed_sequence.cpp:19-29)
+    t[3000, 90] = ord("X")       # same pair: text is checked before pattern
+    p[4000, 3] = 0
+    with pytest.raises(gpu.illegal_character_error) as ei:
+        gpu.shouji_filter_batch(t, p, 5)
+    err = ei.value
+    assert (err.pair, err.field, err.position(), err.byte()) == (3000, 0, 90, "X")
+    t[3000, 90] = ord("A")
+    with pytest.raises(gpu.illegal_character_error) as ei:
+        gpu.shouji_filter_batch(t, p, 5)
+    assert (ei.value.pair, ei.value.field, ei.value.position(), ei.value.byte()) == (3000, 1, 17, "a")
+    # also reported with e >= m (packing precedes the short-circuit) and a bad width
+    with pytest.raises(gpu.illegal_character_error):
+        gpu.shouji_filter_batch(t, p, 500)
+    with pytest.raises(gpu.illegal_character_error):
+        gpu.shouji_filter_batch(t, p, 5, width=9)
+    # every other byte value is rejected too
+    for b in [0, 1, 64, 66, 0x61, 0x6E, 0xC1, 0xFF, ord("U"), ord("n")]:
+        q = t[:64].copy()
+        q[63, 99] = b
+        with pytest.raises(gpu.illegal_character_error):
+            gpu.shouji_filter_batch(q, t[:64], 5)
+
+
+def test_empty_sequence(gpu):
+    with pytest.raises(gpu.empty_sequence_error):
+        gpu.shouji_filter_batch(np.zeros((4, 0), np.uint8), np.zeros((4, 0), np.uint8), 1, m=0)
+    with pytest.raises(gpu.empty_sequence_error):
+        gpu.seq("")
+
+
+# --- mutation tests: the harness catches a wrong rule -------------------------------
+
+def test_mutations_are_caught(gpu, oracle):
+    t, p = oracle.generate_pairs(5, 50_000, 100, 0, 10)
+    acc, est, _ = gpu.shouji_filter_batch(t, p, 5, estimates=True)
+    a0, e0, _ = oracle.shouji_batch(t, p, 5)
+    assert (acc == a0).all() and (est == e0).all()
+    try:
+        for v in (1, 2, 3, 4):
+            oracle.set_variant(v)
+            av, ev, _ = oracle.shouji_batch(t, p, 5)
+            assert (ev != est).sum() > 100, v  # a wrong rule would not pass parity
+    finally:
+        oracle.set_variant(0)
+
+
+# --- multi-device sharding logic on one GPU -----------------------------------------
+
+def test_context_sharding(gpu, oracle):
+    t, p = oracle.generate_pairs(11, 100_003, 100, 0, 10)
+    ref_a, ref_e, _ = oracle.shouji_batch(t, p, 5)
+    for devs in ([0, 0], [0, 0, 0]):
+        ctx = gpu.Context(devs)
+        assert ctx.device_count() == len(devs)
+        a, e, _ = gpu.shouji_filter_batch(t, p, 5, estimates=True, ctx=ctx)
+        assert (a == ref_a).all() and (e == ref_e).all()
+        p2 = p.copy()
+        p2[70_000, 5] = ord("Z")
+        p2[90_000, 5] = ord("Z")
+        with pytest.raises(gpu.illegal_character_error) as ei:
+            gpu.shouji_filter_batch(t, p2, 5, ctx=ctx)
+        assert ei.value.pair == 70_000
+        ctx.close()
+
+
+def test_pinned_host_buffers(gpu, oracle):
+    import torch
+    t, p = oracle.generate_pairs(12, 50_000, 100, 0, 10)
+    tp = torch.from_numpy(t).pin_memory()
+    pp = torch.from_numpy(p).pin_memory()
+    a, e, _ = gpu.shouji_filter_batch(tp.numpy(), pp.numpy(), 5, estimates=True)
+    a2, e2, _ = oracle.shouji_batch(t, p, 5)
+    assert (a == a2).all() and (e == e2).all()
