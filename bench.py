@@ -253,7 +253,9 @@ def run_ours(args, rank, world, local_rank):
     ctx = pf.Context([local_rank])
     n, m, e = args.pairs, args.m, args.e
     pitch = pf.device_pitch(m)
-    stream = torch.cuda.current_stream(dev)
+    # A dedicated stream: the kernels and the timing events must share it.
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
 
     # ---- workload: configs[1] at E on this rank's device ---------------------------

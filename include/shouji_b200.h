@@ -102,7 +102,7 @@ int pf_shouji_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* patt
                            pf_error* err);
 
 /* Same over DEVICE-resident records on the ctx's first device, asynchronous
- * on `stream` (a cudaStream_t; NULL = the ctx stream) except that an error
+ * on `stream` (a cudaStream_t; NULL = the legacy default stream) except that an error
  * check forces a stream synchronisation at the end. Records must use
  * pf_device_pitch(m) bytes per row and 16-byte aligned bases (so every row
  * starts 16-byte aligned); bytes in [m, pitch) are ignored. Output pointers

@@ -21,7 +21,7 @@
 
 namespace {
 
-constexpr size_t kStageRows = 1 << 18;  // pairs per pinned staging chunk (pageable input)
+constexpr size_t kStageBytes = size_t(64) << 20;  // per-sequence H2D staging chunk
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -44,6 +44,8 @@ struct DeviceState {
     size_t scratch_words = 0;
     uint32_t* d_flag = nullptr;
     unsigned long long* d_key = nullptr;
+    uint8_t* d_stage = nullptr;  // device staging for non-pitched host rows
+    size_t d_stage_bytes = 0;
     uint8_t* h_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
@@ -169,49 +171,76 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     }
 
     // ---- host -> device ----------------------------------------------------
+    // Records land in the device layout (pitch = round16(m)). A caller buffer
+    // already in that layout is one DMA per sequence; otherwise rows are
+    // streamed in chunks: contiguous DMA of the caller's rows into a device
+    // staging slot, then a repitch kernel. Pageable input first goes through a
+    // double-buffered pinned staging copy (host memcpy of chunk i+1 overlaps the
+    // DMA of chunk i).
     const uint8_t* tsrc = text + p0 * stride;
     const uint8_t* psrc = pattern + p0 * stride;
-    if (is_pinned(text) && is_pinned(pattern)) {
-        if (!cu(cudaMemcpy2DAsync(d.d_text, pitch, tsrc, stride, m, n, cudaMemcpyHostToDevice,
-                                  d.stream), "H2D text"))
+    const bool pinned = is_pinned(text) && is_pinned(pattern);
+    if (pinned && stride == pitch) {
+        const size_t bytes = (n - 1) * pitch + m;
+        if (!cu(cudaMemcpyAsync(d.d_text, tsrc, bytes, cudaMemcpyHostToDevice, d.stream), "H2D text"))
             return;
-        if (!cu(cudaMemcpy2DAsync(d.d_pattern, pitch, psrc, stride, m, n, cudaMemcpyHostToDevice,
-                                  d.stream), "H2D pattern"))
+        if (!cu(cudaMemcpyAsync(d.d_pattern, psrc, bytes, cudaMemcpyHostToDevice, d.stream),
+                "H2D pattern"))
             return;
     } else {
-        // pageable: double-buffered pinned staging, host copy of chunk i+1
-        // overlaps the DMA of chunk i.
-        const size_t rows = std::min(n, kStageRows);
-        const size_t need = rows * m * 2;
-        if (d.stage_bytes < need) {
-            for (int b = 0; b < 2; ++b) {
-                if (d.h_stage[b]) cudaFreeHost(d.h_stage[b]);
-                d.h_stage[b] = nullptr;
-                if (!cu(cudaHostAlloc(&d.h_stage[b], need, cudaHostAllocPortable), "alloc stage"))
-                    return;
-                if (!d.stage_ev[b] &&
-                    !cu(cudaEventCreateWithFlags(&d.stage_ev[b], cudaEventDisableTiming), "event"))
-                    return;
+        const size_t sstride = pinned ? stride : m;  // row stride of what is DMA'd
+        const size_t rows = std::max<size_t>(1, std::min(n, kStageBytes / sstride));
+        if (!cu(grow(d.d_stage, d.d_stage_bytes, 2 * rows * sstride), "alloc device stage")) return;
+        if (!pinned) {
+            const size_t need = rows * m * 2;
+            if (d.stage_bytes < need) {
+                for (int b = 0; b < 2; ++b) {
+                    if (d.h_stage[b]) cudaFreeHost(d.h_stage[b]);
+                    d.h_stage[b] = nullptr;
+                    if (!cu(cudaHostAlloc(&d.h_stage[b], need, cudaHostAllocPortable), "alloc stage"))
+                        return;
+                    if (!d.stage_ev[b] &&
+                        !cu(cudaEventCreateWithFlags(&d.stage_ev[b], cudaEventDisableTiming), "event"))
+                        return;
+                }
+                d.stage_bytes = need;
             }
-            d.stage_bytes = need;
         }
         int buf = 0;
         for (size_t r0 = 0; r0 < n; r0 += rows, buf ^= 1) {
             const size_t nr = std::min(rows, n - r0);
-            if (!cu(cudaEventSynchronize(d.stage_ev[buf]), "stage wait")) return;
-            uint8_t* st = d.h_stage[buf];
-            uint8_t* sp = st + rows * m;
-            for (size_t r = 0; r < nr; ++r) {
-                std::memcpy(st + r * m, tsrc + (r0 + r) * stride, m);
-                std::memcpy(sp + r * m, psrc + (r0 + r) * stride, m);
+            const uint8_t* st;
+            const uint8_t* sp;
+            if (pinned) {
+                st = tsrc + r0 * stride;
+                sp = psrc + r0 * stride;
+            } else {
+                if (!cu(cudaEventSynchronize(d.stage_ev[buf]), "stage wait")) return;
+                uint8_t* ht = d.h_stage[buf];
+                uint8_t* hp = ht + rows * m;
+                for (size_t r = 0; r < nr; ++r) {
+                    std::memcpy(ht + r * m, tsrc + (r0 + r) * stride, m);
+                    std::memcpy(hp + r * m, psrc + (r0 + r) * stride, m);
+                }
+                st = ht;
+                sp = hp;
             }
-            if (!cu(cudaMemcpy2DAsync(d.d_text + r0 * pitch, pitch, st, m, m, nr,
-                                      cudaMemcpyHostToDevice, d.stream), "H2D text"))
+            const size_t bytes = (nr - 1) * sstride + m;
+            uint8_t* dt = d.d_stage;
+            uint8_t* dp = d.d_stage + rows * sstride;
+            if (!cu(cudaMemcpyAsync(dt, st, bytes, cudaMemcpyHostToDevice, d.stream), "H2D text"))
                 return;
-            if (!cu(cudaMemcpy2DAsync(d.d_pattern + r0 * pitch, pitch, sp, m, m, nr,
-                                      cudaMemcpyHostToDevice, d.stream), "H2D pattern"))
+            if (!cu(cudaMemcpyAsync(dp, sp, bytes, cudaMemcpyHostToDevice, d.stream), "H2D pattern"))
                 return;
-            if (!cu(cudaEventRecord(d.stage_ev[buf], d.stream), "stage record")) return;
+            if (!pinned && !cu(cudaEventRecord(d.stage_ev[buf], d.stream), "stage record")) return;
+            if (!cu(sb::launch_repitch(dt, sstride, d.d_text + r0 * pitch, pitch,
+                                       static_cast<long long>(nr), static_cast<int>(m), d.stream),
+                    "repitch text"))
+                return;
+            if (!cu(sb::launch_repitch(dp, sstride, d.d_pattern + r0 * pitch, pitch,
+                                       static_cast<long long>(nr), static_cast<int>(m), d.stream),
+                    "repitch pattern"))
+                return;
         }
     }
 
@@ -368,6 +397,7 @@ void pf_ctx_destroy(pf_ctx* ctx) {
         cudaFree(d.d_scratch);
         cudaFree(d.d_flag);
         cudaFree(d.d_key);
+        cudaFree(d.d_stage);
         for (int b = 0; b < 2; ++b) {
             if (d.h_stage[b]) cudaFreeHost(d.h_stage[b]);
             if (d.stage_ev[b]) cudaEventDestroy(d.stage_ev[b]);
@@ -451,7 +481,7 @@ int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceState& d = ctx->devs[0];
     PF_CUDA(cudaSetDevice(d.device));
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t ngroups = (n + 31) / 32;
     if (!d.d_flag) {
         PF_CUDA(cudaMalloc(&d.d_flag, sizeof(uint32_t)));
@@ -522,7 +552,7 @@ int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceState& d = ctx->devs[0];
     PF_CUDA(cudaSetDevice(d.device));
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!sb::use_fused(width, e, static_cast<int>(m)))
         PF_CUDA(grow(d.d_scratch, d.scratch_words,
                      sb::generic_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
@@ -622,7 +652,7 @@ int pf_generate_device(pf_ctx* ctx, int kind, uint64_t seed, uint32_t param, uin
     pf_error* err = nullptr;
     DeviceState& d = ctx->devs[0];
     PF_CUDA(cudaSetDevice(d.device));
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d.stream;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
     const cudaError_t st = sb::launch_generate(kind, seed, param, d_text, d_pattern, pitch,
                                                static_cast<long long>(n), static_cast<int>(m), s);
     if (st == cudaErrorInvalidValue) return PF_ERR_INVALID_PARAMETERS;

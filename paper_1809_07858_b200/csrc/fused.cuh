@@ -131,7 +131,9 @@ shouji_fused_w4(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pa
     for (int i = 0; i < NC; ++i) cnt[i] = 0u;
 
     const int C = (m + 3 + CH - 1) / CH;  // chunks: windows must reach m-1
-    for (int t = -L; t < C; ++t) {
+    // t < 0 only primes the rings: pattern chunks -L..L-1 (negative = all N)
+    // and, without CARRY, text chunk -1.
+    for (int t = -2 * L; t < C; ++t) {
         // ---- phase A: pattern chunk t+L, text chunk t (one inlined gather) --
 #pragma unroll 1
         for (int sidx = 0; sidx < 2; ++sidx) {

@@ -336,6 +336,33 @@ cudaError_t launch_bits_transpose(const uint32_t* outplanes, long long n, int m,
     return cudaGetLastError();
 }
 
+// One thread per 4-byte output word; consecutive threads read consecutive
+// source bytes, so the byte loads coalesce.
+__global__ void repitch_kernel(const uint8_t* __restrict__ src, size_t src_stride,
+                               uint8_t* __restrict__ dst, size_t dst_pitch, long long n, int m) {
+    const int wpr = (m + 3) / 4;
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n * wpr) return;
+    const long long row = i / wpr;
+    const int c0 = static_cast<int>(i % wpr) * 4;
+    const uint8_t* s = src + row * src_stride + c0;
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (c0 + k < m) v |= static_cast<uint32_t>(__ldg(s + k)) << (8 * k);
+    *reinterpret_cast<uint32_t*>(dst + row * dst_pitch + c0) = v;
+}
+
+cudaError_t launch_repitch(const uint8_t* src, size_t src_stride, uint8_t* dst, size_t dst_pitch,
+                           long long n, int m, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const long long total = n * ((m + 3) / 4);
+    const unsigned grid = static_cast<unsigned>((total + 255) / 256);
+    repitch_kernel<<<grid, 256, 0, s>>>(src, src_stride, dst, dst_pitch, n, m);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_accept_all(long long n, int m, uint32_t* accept, uint32_t* estimates,
                               uint64_t* bits, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
