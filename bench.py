@@ -384,7 +384,9 @@ def run_ours(args, rank, world, local_rank):
                 "unit": "GB/s", "frac": achieved_gbs / float(peaks["hbm_gbs"]), "traffic": traffic,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
                 "algorithmic_bytes_per_pair": 2 * m + 1 / 8,
-                "kernel": "sb::shouji_fused_w4<5> (fused pack+map+search+commit+accept)",
+                "kernels": "sb::pack_tile_kernel (TMA records -> planes, validation) + "
+                           "sb::shouji_search_w4<5> (map+search+commit+accept); achieved is over "
+                           "the whole step (both launches)",
                 "kernel_ms_avg": kern_avg_ms}
     int_view = None
     if rank == 0:

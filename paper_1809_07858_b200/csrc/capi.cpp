@@ -160,10 +160,9 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         if (!cu(grow(d.d_outplanes, d.outplanes_words, size_t(m) * ngroups), "alloc tally planes"))
             return;
     }
-    const bool fused = sb::use_fused(width, e, static_cast<int>(m));
-    if (!fused && e < m && width >= 3 && width <= 8) {
-        const size_t need = sb::generic_scratch_words(static_cast<long long>(n), static_cast<int>(m));
-        if (!cu(grow(d.d_scratch, d.scratch_words, need), "alloc scratch")) return;
+    if (e < m && width >= 3 && width <= 8) {
+        const size_t need = sb::planes_scratch_words(static_cast<long long>(n), static_cast<int>(m));
+        if (!cu(grow(d.d_scratch, d.scratch_words, need), "alloc planes")) return;
     }
     if (!d.d_flag) {
         if (!cu(cudaMalloc(&d.d_flag, sizeof(uint32_t)), "alloc flag")) return;
@@ -258,8 +257,8 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     a.estimates = estimates ? d.d_est : nullptr;
     a.outplanes = bits ? d.d_outplanes : nullptr;
     a.err_flag = d.d_flag;
-    a.scratch = d.d_scratch;
-    a.scratch_words = d.scratch_words;
+    a.planes = d.d_scratch;
+    a.planes_words = d.scratch_words;
     const bool short_circuit = e >= m;
     const bool bad_width = width < 3 || width > 8;
     if (short_circuit || bad_width) {
@@ -487,10 +486,9 @@ int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
         PF_CUDA(cudaMalloc(&d.d_flag, sizeof(uint32_t)));
         PF_CUDA(cudaMalloc(&d.d_key, sizeof(unsigned long long)));
     }
-    const bool fused = sb::use_fused(width, e, static_cast<int>(m));
-    if (!fused && e < m && width >= 3 && width <= 8)
+    if (e < m && width >= 3 && width <= 8)
         PF_CUDA(grow(d.d_scratch, d.scratch_words,
-                     sb::generic_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
+                     sb::planes_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
     if (d_bits) PF_CUDA(grow(d.d_outplanes, d.outplanes_words, size_t(m) * ngroups));
     PF_CUDA(cudaMemsetAsync(d.d_flag, 0, sizeof(uint32_t), s));
     sb::FilterArgs a{};
@@ -505,8 +503,8 @@ int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
     a.estimates = d_estimates;
     a.outplanes = d_bits ? d.d_outplanes : nullptr;
     a.err_flag = d.d_flag;
-    a.scratch = d.d_scratch;
-    a.scratch_words = d.scratch_words;
+    a.planes = d.d_scratch;
+    a.planes_words = d.scratch_words;
     const bool short_circuit = e >= m;
     const bool bad_width = width < 3 || width > 8;
     if (short_circuit || bad_width)
@@ -553,9 +551,8 @@ int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint
     DeviceState& d = ctx->devs[0];
     PF_CUDA(cudaSetDevice(d.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!sb::use_fused(width, e, static_cast<int>(m)))
-        PF_CUDA(grow(d.d_scratch, d.scratch_words,
-                     sb::generic_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
+    PF_CUDA(grow(d.d_scratch, d.scratch_words,
+                 sb::planes_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
     sb::FilterArgs a{};
     a.text = d_text;
     a.pattern = d_pattern;
@@ -568,8 +565,8 @@ int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint
     a.estimates = d_estimates;
     a.outplanes = nullptr;
     a.err_flag = d_err_flag;
-    a.scratch = d.d_scratch;
-    a.scratch_words = d.scratch_words;
+    a.planes = d.d_scratch;
+    a.planes_words = d.scratch_words;
     PF_CUDA(sb::launch_filter(a, s));
     return PF_OK;
 }

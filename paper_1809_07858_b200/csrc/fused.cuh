@@ -5,13 +5,12 @@
 // select_window (shouji.cpp:17-31) and commit_window (shouji.cpp:33-39), and
 // finally accept iff popcount(bv) <= E (shouji.cpp:56-57).
 //
-// One thread owns 32 consecutive pairs (pair-sliced words, see phase_a.cuh).
-// Per 16-column chunk the thread gathers the text chunk and a look-ahead
-// pattern chunk into a thread-private shared-memory ring (phase A), then runs
-// four blocks of four windows (phase B):
+// One thread owns one group of 32 consecutive pairs and reads the group's
+// pair-sliced planes (written by the pack kernel, pack.cuh) column by column.
+// Per block of four windows:
 //   * the diagonal loop d = -E..+E is fully unrolled and scanned in reference
-//     order; each new pattern column is one LDS per plane, kept in a sliding
-//     register window;
+//     order; each new pattern column is one load per plane (8 threads share
+//     one fully used 32-byte sector), kept in a sliding register window;
 //   * D_d for the block's columns is (Plo^Tlo)|(Phi^Thi)|PN|TN;
 //   * the window key is 2*ones + bit0 and the winner is the strict first
 //     minimum — exactly select_window's "more zeros, or equal zeros and a
@@ -31,6 +30,7 @@
 
 #include "bitslice.cuh"
 #include "kernels.cuh"
+#include "pack.cuh"
 #include "phase_a.cuh"
 
 namespace sb {
@@ -76,51 +76,45 @@ __device__ __forceinline__ uint32_t fsm_step4(const Cand4& best, uint32_t (&S)[3
 }
 
 template <int E>
-struct FusedCfg {
+struct SearchCfg {
     static constexpr bool CARRY = E <= 12;
-    static constexpr int B = 4;                     // windows per block
-    static constexpr int LOOK = CARRY ? E : E + 3;  // pattern reach beyond the chunk
-    static constexpr int L = (LOOK + CH - 1) / CH;  // look-ahead chunks
-    static constexpr int R = 2 * L + 1;             // pattern ring slots
-    static constexpr int TR = CARRY ? 1 : 2;        // text ring slots
-    static constexpr int COLS = (TR + R) * CH;
-    static constexpr int BYTES_PER_THREAD = COLS * 3 * 4;
-    static constexpr int NT = BYTES_PER_THREAD * 128 <= 100 * 1024   ? 128
-                              : BYTES_PER_THREAD * 64 <= 100 * 1024 ? 64
-                                                                     : 32;
-    static constexpr size_t SMEM = size_t(BYTES_PER_THREAD) * NT;
+    static constexpr int B = 4;  // windows per block
+    static constexpr int NT = 128;
 };
 
+// Planes of one group, one sequence: column `col` plane k at base[(col*3+k)*8].
+// Columns outside [0, m) read as N (lo = hi = 0, N = 1).
+__device__ __forceinline__ void load_col(const uint32_t* __restrict__ base, int col, int m,
+                                         uint32_t (&v)[3]) {
+    if (static_cast<unsigned>(col) < static_cast<unsigned>(m)) {
+        v[0] = __ldg(base + (col * 3 + 0) * kPackGroups);
+        v[1] = __ldg(base + (col * 3 + 1) * kPackGroups);
+        v[2] = __ldg(base + (col * 3 + 2) * kPackGroups);
+    } else {
+        v[0] = 0u;
+        v[1] = 0u;
+        v[2] = ~0u;
+    }
+}
+
 template <int E>
-__global__ void __launch_bounds__(FusedCfg<E>::NT)
-shouji_fused_w4(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
-                size_t pitch, long long n, int m, uint32_t* __restrict__ accept,
-                uint32_t* __restrict__ estimates, uint32_t* __restrict__ outplanes,
-                uint32_t* __restrict__ err_flag) {
-    using Cfg = FusedCfg<E>;
-    constexpr int NT = Cfg::NT, L = Cfg::L, R = Cfg::R, TR = Cfg::TR, B = Cfg::B;
+__global__ void __launch_bounds__(SearchCfg<E>::NT)
+shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
+                 uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
+                 uint32_t* __restrict__ outplanes) {
+    using Cfg = SearchCfg<E>;
+    constexpr int NT = Cfg::NT, B = Cfg::B;
     constexpr bool CARRY = Cfg::CARRY;
     constexpr int NC = 8;  // counter planes: estimates up to 255 (m <= 255 here)
-    extern __shared__ uint32_t smem[];
-    const int tid = threadIdx.x;
-    const long long g = static_cast<long long>(blockIdx.x) * NT + tid;
+    const long long g = static_cast<long long>(blockIdx.x) * NT + threadIdx.x;
     const long long row0 = g * 32;
     if (row0 >= n) return;
     const long long ngroups = (n + 31) / 32;
+    const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
+    const int mc = plane_cols(m);
+    const uint32_t* const tb = planes + plane_index(0, g, 0, 0, nblocks, mc);
+    const uint32_t* const pb = planes + plane_index(1, g, 0, 0, nblocks, mc);
 
-    uint32_t* const tring = smem + tid;                 // [TR*CH][3][NT]
-    uint32_t* const pring = smem + TR * CH * 3 * NT + tid;  // [R*CH][3][NT]
-    // Ring addressing: chunk q lives in slot q mod R (q >= -R*4 kept positive).
-    auto pcol = [&](int col) -> const uint32_t* {
-        const int q = (col + CH * R * 4) / CH;
-        return pring + (((q % R) * CH + (col & (CH - 1))) * 3) * NT;
-    };
-    auto tcol = [&](int col) -> const uint32_t* {
-        const int q = (col + CH * TR * 4) / CH;
-        return tring + (((q % TR) * CH + (col & (CH - 1))) * 3) * NT;
-    };
-
-    uint32_t err = 0u;
     constexpr int DCN = CARRY ? 2 * E + 1 : 1;
     uint32_t Dc[DCN][3];
 #pragma unroll
@@ -130,150 +124,107 @@ shouji_fused_w4(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pa
 #pragma unroll
     for (int i = 0; i < NC; ++i) cnt[i] = 0u;
 
-    const int C = (m + 3 + CH - 1) / CH;  // chunks: windows must reach m-1
-    // t < 0 only primes the rings: pattern chunks -L..L-1 (negative = all N)
-    // and, without CARRY, text chunk -1.
-    for (int t = -2 * L; t < C; ++t) {
-        // ---- phase A: pattern chunk t+L, text chunk t (one inlined gather) --
+    const int NB = (m + 3 + B - 1) / B;  // blocks: windows must reach m-1
 #pragma unroll 1
-        for (int sidx = 0; sidx < 2; ++sidx) {
-            const bool pat = sidx == 0;
-            const int q = pat ? t + L : t;
-            if (!pat && q < -(TR - 1)) break;
-            uint32_t* dst = pat ? pring + ((((q % R) + R) % R) * CH * 3) * NT
-                                : tring + ((((q % TR) + TR) % TR) * CH * 3) * NT;
-            err |= produce_chunk(pat ? pattern : text, pitch, row0, n, q, m, dst, NT);
-        }
-        if (t < 0) continue;
-        const int c = t;
-        // ---- phase B ---------------------------------------------------------
-#pragma unroll 1
-        for (int blk = 0; blk < CH / B; ++blk) {
-            const int j0 = c * CH - 3 + blk * B;  // first window of the block
-            Cand4 best[B];
-            if constexpr (CARRY) {
-                // new D columns j0+3 .. j0+3+B-1; pattern column = that + d
-                uint32_t T[B][3];
+    for (int blk = 0; blk < NB; ++blk) {
+        const int j0 = blk * B - 3;  // first window of the block
+        Cand4 best[B];
+        if constexpr (CARRY) {
+            // new D columns j0+3 .. j0+3+B-1; pattern column = that + d
+            uint32_t T[B][3];
+#pragma unroll
+            for (int b = 0; b < B; ++b) load_col(tb, j0 + 3 + b, m, T[b]);
+            uint32_t P[B][3];
+#pragma unroll
+            for (int di = 0; di <= 2 * E; ++di) {
+                if (di == 0) {
+#pragma unroll
+                    for (int b = 0; b < B; ++b) load_col(pb, j0 + 3 + b - E, m, P[b]);
+                } else {
+#pragma unroll
+                    for (int b = 0; b < B - 1; ++b) {
+                        P[b][0] = P[b + 1][0];
+                        P[b][1] = P[b + 1][1];
+                        P[b][2] = P[b + 1][2];
+                    }
+                    load_col(pb, j0 + 3 + B - 1 - E + di, m, P[B - 1]);
+                }
+                uint32_t s[B + 3];
+                s[0] = Dc[CARRY ? di : 0][0];
+                s[1] = Dc[CARRY ? di : 0][1];
+                s[2] = Dc[CARRY ? di : 0][2];
+#pragma unroll
+                for (int b = 0; b < B; ++b)
+                    s[3 + b] = (P[b][0] ^ T[b][0]) | (P[b][1] ^ T[b][1]) | P[b][2] | T[b][2];
 #pragma unroll
                 for (int b = 0; b < B; ++b) {
-                    const uint32_t* p = tcol(j0 + 3 + b);
-                    T[b][0] = p[0];
-                    T[b][1] = p[NT];
-                    T[b][2] = p[2 * NT];
+                    Cand4 cd;
+                    make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
+                    if (di == 0)
+                        best[b] = cd;
+                    else
+                        update_best4(cd, best[b]);
                 }
-                uint32_t P[B][3];
+                Dc[CARRY ? di : 0][0] = s[B];
+                Dc[CARRY ? di : 0][1] = s[B + 1];
+                Dc[CARRY ? di : 0][2] = s[B + 2];
+            }
+        } else {
+            // D over columns j0 .. j0+B+2 rebuilt per block.
+            constexpr int X = B + 3;
+            uint32_t T[X][3];
 #pragma unroll
-                for (int di = 0; di <= 2 * E; ++di) {
-                    if (di == 0) {
+            for (int x = 0; x < X; ++x) load_col(tb, j0 + x, m, T[x]);
+            uint32_t P[X][3];
 #pragma unroll
-                        for (int b = 0; b < B; ++b) {
-                            const uint32_t* p = pcol(j0 + 3 + b - E);
-                            P[b][0] = p[0];
-                            P[b][1] = p[NT];
-                            P[b][2] = p[2 * NT];
-                        }
-                    } else {
+            for (int di = 0; di <= 2 * E; ++di) {
+                if (di == 0) {
 #pragma unroll
-                        for (int b = 0; b < B - 1; ++b) {
-                            P[b][0] = P[b + 1][0];
-                            P[b][1] = P[b + 1][1];
-                            P[b][2] = P[b + 1][2];
-                        }
-                        const uint32_t* p = pcol(j0 + 3 + B - 1 - E + di);
-                        P[B - 1][0] = p[0];
-                        P[B - 1][1] = p[NT];
-                        P[B - 1][2] = p[2 * NT];
+                    for (int x = 0; x < X; ++x) load_col(pb, j0 + x - E, m, P[x]);
+                } else {
+#pragma unroll
+                    for (int x = 0; x < X - 1; ++x) {
+                        P[x][0] = P[x + 1][0];
+                        P[x][1] = P[x + 1][1];
+                        P[x][2] = P[x + 1][2];
                     }
-                    uint32_t s[B + 3];
-                    s[0] = Dc[CARRY ? di : 0][0];
-                    s[1] = Dc[CARRY ? di : 0][1];
-                    s[2] = Dc[CARRY ? di : 0][2];
-#pragma unroll
-                    for (int b = 0; b < B; ++b)
-                        s[3 + b] = (P[b][0] ^ T[b][0]) | (P[b][1] ^ T[b][1]) | P[b][2] | T[b][2];
-#pragma unroll
-                    for (int b = 0; b < B; ++b) {
-                        Cand4 cd;
-                        make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
-                        if (di == 0)
-                            best[b] = cd;
-                        else
-                            update_best4(cd, best[b]);
-                    }
-                    Dc[CARRY ? di : 0][0] = s[B];
-                    Dc[CARRY ? di : 0][1] = s[B + 1];
-                    Dc[CARRY ? di : 0][2] = s[B + 2];
+                    load_col(pb, j0 + X - 1 - E + di, m, P[X - 1]);
                 }
-            } else {
-                // D over columns j0 .. j0+B+2 rebuilt per block.
-                constexpr int X = B + 3;
-                uint32_t T[X][3];
+                uint32_t s[X];
 #pragma unroll
-                for (int x = 0; x < X; ++x) {
-                    const uint32_t* p = tcol(j0 + x);
-                    T[x][0] = p[0];
-                    T[x][1] = p[NT];
-                    T[x][2] = p[2 * NT];
-                }
-                uint32_t P[X][3];
+                for (int x = 0; x < X; ++x)
+                    s[x] = (P[x][0] ^ T[x][0]) | (P[x][1] ^ T[x][1]) | P[x][2] | T[x][2];
 #pragma unroll
-                for (int di = 0; di <= 2 * E; ++di) {
-                    if (di == 0) {
-#pragma unroll
-                        for (int x = 0; x < X; ++x) {
-                            const uint32_t* p = pcol(j0 + x - E);
-                            P[x][0] = p[0];
-                            P[x][1] = p[NT];
-                            P[x][2] = p[2 * NT];
-                        }
-                    } else {
-#pragma unroll
-                        for (int x = 0; x < X - 1; ++x) {
-                            P[x][0] = P[x + 1][0];
-                            P[x][1] = P[x + 1][1];
-                            P[x][2] = P[x + 1][2];
-                        }
-                        const uint32_t* p = pcol(j0 + X - 1 - E + di);
-                        P[X - 1][0] = p[0];
-                        P[X - 1][1] = p[NT];
-                        P[X - 1][2] = p[2 * NT];
-                    }
-                    uint32_t s[X];
-#pragma unroll
-                    for (int x = 0; x < X; ++x)
-                        s[x] = (P[x][0] ^ T[x][0]) | (P[x][1] ^ T[x][1]) | P[x][2] | T[x][2];
-#pragma unroll
-                    for (int b = 0; b < B; ++b) {
-                        Cand4 cd;
-                        make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
-                        if (di == 0)
-                            best[b] = cd;
-                        else
-                            update_best4(cd, best[b]);
-                    }
+                for (int b = 0; b < B; ++b) {
+                    Cand4 cd;
+                    make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
+                    if (di == 0)
+                        best[b] = cd;
+                    else
+                        update_best4(cd, best[b]);
                 }
             }
-            // commit chain over the block's windows, in column order
-            uint32_t outs[B];
-#pragma unroll
-            for (int b = 0; b < B; ++b) {
-                const int j = j0 + b;
-                outs[b] = 0u;
-                if (j >= 0 && j < m) {
-                    outs[b] = fsm_step4(best[b], S);
-                    if (outplanes) outplanes[static_cast<long long>(j) * ngroups + g] = outs[b];
-                }
-            }
-            uint32_t v[3];
-            {
-                const uint32_t s1 = outs[0] ^ outs[1] ^ outs[2];
-                const uint32_t c1 = (outs[0] & outs[1]) | (outs[0] & outs[2]) | (outs[1] & outs[2]);
-                v[0] = s1 ^ outs[3];
-                v[1] = c1 ^ (s1 & outs[3]);
-                v[2] = c1 & s1 & outs[3];
-            }
-            bs_add(cnt, v);
         }
+        // commit chain over the block's windows, in column order
+        uint32_t outs[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const int j = j0 + b;
+            outs[b] = 0u;
+            if (j >= 0 && j < m) {
+                outs[b] = fsm_step4(best[b], S);
+                if (outplanes) outplanes[static_cast<long long>(j) * ngroups + g] = outs[b];
+            }
+        }
+        uint32_t v[3];
+        {
+            const uint32_t s1 = outs[0] ^ outs[1] ^ outs[2];
+            const uint32_t c1 = (outs[0] & outs[1]) | (outs[0] & outs[2]) | (outs[1] & outs[2]);
+            v[0] = s1 ^ outs[3];
+            v[1] = c1 ^ (s1 & outs[3]);
+            v[2] = c1 & s1 & outs[3];
+        }
+        bs_add(cnt, v);
     }
 
     // accept = ones <= e (shouji.cpp:56-57); bits of pairs past n are 0.
@@ -289,24 +240,15 @@ shouji_fused_w4(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pa
             estimates[row0 + b] = est;
         }
     }
-    if (err) atomicOr(err_flag, 1u);
 }
 
 template <int E>
-cudaError_t launch_fused_e(const FilterArgs& a, cudaStream_t s) {
-    using Cfg = FusedCfg<E>;
-    auto kern = shouji_fused_w4<E>;
-    static bool attr_set = false;  // per instantiation; the call is idempotent
-    if (!attr_set) {
-        cudaError_t st = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(Cfg::SMEM));
-        if (st != cudaSuccess) return st;
-        attr_set = true;
-    }
+cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s) {
+    using Cfg = SearchCfg<E>;
     const long long ngroups = (a.n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + Cfg::NT - 1) / Cfg::NT);
-    kern<<<grid, Cfg::NT, Cfg::SMEM, s>>>(a.text, a.pattern, a.pitch, a.n, a.m, a.accept,
-                                          a.estimates, a.outplanes, a.err_flag);
+    shouji_search_w4<E><<<grid, Cfg::NT, 0, s>>>(a.planes, a.n, a.m, a.accept, a.estimates,
+                                                  a.outplanes);
     count_launch();
     return cudaGetLastError();
 }
@@ -315,4 +257,4 @@ cudaError_t launch_fused_e(const FilterArgs& a, cudaStream_t s) {
 
 // Explicit instantiation helper for the fused_e*.cu units.
 #define SB_INSTANTIATE_FUSED(E) \
-    template cudaError_t sb::launch_fused_e<E>(const sb::FilterArgs&, cudaStream_t);
+    template cudaError_t sb::launch_search_e<E>(const sb::FilterArgs&, cudaStream_t);

@@ -32,6 +32,7 @@
 
 #include "bitslice.cuh"
 #include "kernels.cuh"
+#include "pack.cuh"
 #include "phase_a.cuh"
 
 #include <array>
@@ -47,28 +48,6 @@ void count_launch(int k) { g_launches.fetch_add(static_cast<uint64_t>(k)); }
 // Generic path: any width 3..8, any e < m. Two kernels: pack (phase A into
 // global planes [col][3][ngroups]) and a plain pair-sliced sweep reading them.
 // ---------------------------------------------------------------------------
-constexpr int kPackNT = 128;
-
-__global__ void __launch_bounds__(kPackNT)
-pack_planes(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern, size_t pitch,
-            long long n, int m, uint32_t* __restrict__ tplanes, uint32_t* __restrict__ pplanes,
-            uint32_t* __restrict__ err_flag) {
-    const long long g = static_cast<long long>(blockIdx.x) * kPackNT + threadIdx.x;
-    const long long ngroups = (n + 31) / 32;
-    if (g >= ngroups) return;
-    const long long row0 = g * 32;
-    uint32_t err = 0u;
-    const int C = (m + CH - 1) / CH;
-    for (int c = 0; c < C; ++c) {
-        // columns >= m of the last chunk land in the scratch padding (C*CH columns)
-        err |= produce_chunk(text, pitch, row0, n, c, m, tplanes + (size_t(c) * CH * 3) * ngroups + g,
-                             static_cast<int>(ngroups));
-        err |= produce_chunk(pattern, pitch, row0, n, c, m,
-                             pplanes + (size_t(c) * CH * 3) * ngroups + g, static_cast<int>(ngroups));
-    }
-    if (err) atomicOr(err_flag, 1u);
-}
-
 template <int W>
 struct WCfg {
     static constexpr int NO = W >= 8 ? 4 : (W >= 4 ? 3 : 2);  // planes for ones in [0, W]
@@ -78,16 +57,20 @@ struct WCfg {
 
 template <int W, int NC>
 __global__ void __launch_bounds__(128)
-shouji_generic(const uint32_t* __restrict__ tplanes, const uint32_t* __restrict__ pplanes,
-               long long n, int m, int e, uint32_t* __restrict__ accept,
-               uint32_t* __restrict__ estimates, uint32_t* __restrict__ outplanes) {
+shouji_generic(const uint32_t* __restrict__ planes, long long n, int m, int e,
+               uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
+               uint32_t* __restrict__ outplanes) {
     using Cfg = WCfg<W>;
     const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long ngroups = (n + 31) / 32;
     if (g >= ngroups) return;
     const long long row0 = g * 32;
-    auto tp = [&](int col, int k) { return tplanes[(size_t(col) * 3 + k) * ngroups + g]; };
-    auto pp = [&](int col, int k) { return pplanes[(size_t(col) * 3 + k) * ngroups + g]; };
+    const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
+    const int mc = plane_cols(m);
+    const uint32_t* tb = planes + plane_index(0, g, 0, 0, nblocks, mc);
+    const uint32_t* pb = planes + plane_index(1, g, 0, 0, nblocks, mc);
+    auto tp = [&](int col, int k) { return __ldg(tb + (size_t(col) * 3 + k) * kPackGroups); };
+    auto pp = [&](int col, int k) { return __ldg(pb + (size_t(col) * 3 + k) * kPackGroups); };
 
     uint32_t S[W - 1];
 #pragma unroll
@@ -236,28 +219,22 @@ __global__ void accept_all(long long n, int m, uint32_t* accept, uint32_t* estim
 // Defined in fused.cuh, explicitly instantiated in fused_e*.cu (compiled in
 // parallel: each E is its own fully unrolled kernel).
 template <int E>
-cudaError_t launch_fused_e(const FilterArgs& a, cudaStream_t s);
+cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s);
 
-using FusedFn = cudaError_t (*)(const FilterArgs&, cudaStream_t);
+using SearchFn = cudaError_t (*)(const FilterArgs&, cudaStream_t);
 template <int... Es>
-static constexpr std::array<FusedFn, sizeof...(Es)> make_fused_table(std::integer_sequence<int, Es...>) {
-    return {&launch_fused_e<Es>...};
+static constexpr std::array<SearchFn, sizeof...(Es)> make_search_table(std::integer_sequence<int, Es...>) {
+    return {&launch_search_e<Es>...};
 }
-static constexpr auto kFusedTable = make_fused_table(std::make_integer_sequence<int, kFusedMaxE + 1>{});
+static constexpr auto kSearchTable =
+    make_search_table(std::make_integer_sequence<int, kFusedMaxE + 1>{});
 
 template <int W, int NC>
 static cudaError_t launch_generic_w(const FilterArgs& a, cudaStream_t s) {
     const long long ngroups = (a.n + 31) / 32;
-    const int C = (a.m + CH - 1) / CH;
-    uint32_t* tpl = a.scratch;
-    uint32_t* ppl = a.scratch + size_t(C) * CH * 3 * ngroups;
-    const unsigned gp = static_cast<unsigned>((ngroups + kPackNT - 1) / kPackNT);
-    pack_planes<<<gp, kPackNT, 0, s>>>(a.text, a.pattern, a.pitch, a.n, a.m, tpl, ppl, a.err_flag);
-    count_launch();
-    cudaError_t st = cudaGetLastError();
-    if (st != cudaSuccess) return st;
-    shouji_generic<W, NC><<<gp, 128, 0, s>>>(tpl, ppl, a.n, a.m, static_cast<int>(a.e), a.accept,
-                                             a.estimates, a.outplanes);
+    const unsigned grid = static_cast<unsigned>((ngroups + 127) / 128);
+    shouji_generic<W, NC><<<grid, 128, 0, s>>>(a.planes, a.n, a.m, static_cast<int>(a.e), a.accept,
+                                               a.estimates, a.outplanes);
     count_launch();
     return cudaGetLastError();
 }
@@ -275,11 +252,7 @@ static cudaError_t launch_generic(const FilterArgs& a, cudaStream_t s) {
     }
 }
 
-size_t generic_scratch_words(long long n, int m) {
-    const long long ngroups = (n + 31) / 32;
-    const long long C = (m + CH - 1) / CH;
-    return static_cast<size_t>(2 * C * CH * 3 * ngroups);
-}
+size_t planes_scratch_words(long long n, int m) { return plane_words(n, m); }
 
 bool use_fused(uint32_t width, uint32_t e, int m) {
     return width == 4 && e <= static_cast<uint32_t>(kFusedMaxE) && m <= 255;
@@ -287,37 +260,15 @@ bool use_fused(uint32_t width, uint32_t e, int m) {
 
 cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
     if (a.n <= 0) return cudaSuccess;
-    const bool small = a.m <= 255;
-    if (use_fused(a.width, a.e, a.m)) return kFusedTable[a.e](a, s);
-    if (a.scratch == nullptr || a.scratch_words < generic_scratch_words(a.n, a.m))
-        return cudaErrorInvalidValue;
-    return small ? launch_generic<8>(a, s) : launch_generic<24>(a, s);
-}
-
-__global__ void __launch_bounds__(kPackNT)
-validate_only(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern, size_t pitch,
-              long long n, int m, uint32_t* __restrict__ err_flag) {
-    __shared__ uint32_t sink[CH * 3 * kPackNT];
-    const long long g = static_cast<long long>(blockIdx.x) * kPackNT + threadIdx.x;
-    const long long ngroups = (n + 31) / 32;
-    if (g >= ngroups) return;
-    const long long row0 = g * 32;
-    uint32_t err = 0u;
-    const int C = (m + CH - 1) / CH;
-    for (int c = 0; c < C; ++c) {
-        err |= produce_chunk(text, pitch, row0, n, c, m, sink + threadIdx.x, kPackNT);
-        err |= produce_chunk(pattern, pitch, row0, n, c, m, sink + threadIdx.x, kPackNT);
-    }
-    if (err) atomicOr(err_flag, 1u);
+    if (a.planes == nullptr || a.planes_words < plane_words(a.n, a.m)) return cudaErrorInvalidValue;
+    cudaError_t st = launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, a.planes, a.err_flag, s);
+    if (st != cudaSuccess) return st;
+    if (use_fused(a.width, a.e, a.m)) return kSearchTable[a.e](a, s);
+    return a.m <= 255 ? launch_generic<8>(a, s) : launch_generic<24>(a, s);
 }
 
 cudaError_t launch_validate(const FilterArgs& a, cudaStream_t s) {
-    if (a.n <= 0) return cudaSuccess;
-    const long long ngroups = (a.n + 31) / 32;
-    const unsigned gp = static_cast<unsigned>((ngroups + kPackNT - 1) / kPackNT);
-    validate_only<<<gp, kPackNT, 0, s>>>(a.text, a.pattern, a.pitch, a.n, a.m, a.err_flag);
-    count_launch();
-    return cudaGetLastError();
+    return launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, nullptr, a.err_flag, s);
 }
 
 cudaError_t launch_locate(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,

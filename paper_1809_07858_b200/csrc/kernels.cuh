@@ -24,14 +24,18 @@ struct FilterArgs {
     uint32_t* estimates;   // device, n, may be null
     uint32_t* outplanes;   // device scratch [m][ngroups] or null (tally dump)
     uint32_t* err_flag;    // device, 1 word, zeroed by the caller
-    uint32_t* scratch;     // device scratch for the generic path (planes)
-    size_t scratch_words;  // available words in scratch
+    uint32_t* planes;      // device scratch for the pair-sliced planes (pack.cuh)
+    size_t planes_words;   // available words in planes
 };
 
-size_t generic_scratch_words(long long n, int m);
+// Scratch words the filter needs for n pairs of length m.
+size_t planes_scratch_words(long long n, int m);
 bool use_fused(uint32_t width, uint32_t e, int m);
 
-// Launch the filter (fused or generic). Returns a cudaError_t.
+// Stage 1: records -> planes (planes may be null: validation only).
+cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
+                        int m, uint32_t* planes, uint32_t* err_flag, cudaStream_t s);
+// Launch the filter (pack + width-4 search, or pack + generic). Returns a cudaError_t.
 cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s);
 // Validation only (for e >= m or an invalid width): sets *err_flag on any illegal byte.
 cudaError_t launch_validate(const FilterArgs& a, cudaStream_t s);

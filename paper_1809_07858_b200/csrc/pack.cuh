@@ -1,0 +1,48 @@
+// Stage 1 of the Shouji pipeline: ASCII records -> pair-sliced bit planes.
+//
+// Reference: packed_sequence::from_string (proj/src/packed_sequence.cpp:7-34),
+// applied to every text and pattern of the batch before any filtering, as
+// load_pairs / generate_pairs do (proj/src/dataset.cpp:28-30,86-87).
+//
+// Memory shape. One CTA owns a PAIR BLOCK of 256 consecutive pairs (8 groups
+// of 32). Its records are two contiguous byte ranges (256 rows x pitch), so
+// they arrive with two TMA bulk copies (cp.async.bulk, completion on an
+// mbarrier) at full sector efficiency. Threads then bit-transpose 16-column x
+// 32-pair tiles out of shared memory (gather_chunk, phase_a.cuh) and the CTA
+// writes its planes back as one contiguous range per sequence:
+//
+//   planes[s][pair_block][col][plane][8 groups]      (uint32 words)
+//
+// so the filter kernel, whose thread owns one group and walks columns, reads
+// one fully used 32-byte sector per (column, plane) per 8 threads.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "phase_a.cuh"
+
+namespace sb {
+
+constexpr int kPackPairs = 256;                 // pairs per pair block (CTA)
+constexpr int kPackGroups = kPackPairs / 32;    // groups per pair block
+constexpr int kPackNT = 128;                    // threads per pack CTA
+
+// Columns stored per pair (chunk-rounded).
+__host__ __device__ inline int plane_cols(int m) { return (m + CH - 1) / CH * CH; }
+
+// Words of plane storage for n pairs of length m (both sequences).
+inline size_t plane_words(long long n, int m) {
+    const long long blocks = (n + kPackPairs - 1) / kPackPairs;
+    return static_cast<size_t>(2 * blocks * plane_cols(m) * 3 * kPackGroups);
+}
+
+// Offset (in words) of plane word (s, group g, col, k); the group's 8-lane slot is g % 8.
+__host__ __device__ inline size_t plane_index(int s, long long g, int col, int k, long long nblocks,
+                                              int mc) {
+    const long long blk = g / kPackGroups;
+    return ((static_cast<size_t>(s) * nblocks + blk) * mc + col) * (3 * kPackGroups) +
+           k * kPackGroups + (g % kPackGroups);
+}
+
+}  // namespace sb

@@ -73,7 +73,7 @@ __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq
         for (int i = 0; i < 8; ++i) {
             const long long row = row0 + 8 * g8 + i;
             if (row < n)
-                v[i] = __ldg(reinterpret_cast<const uint4*>(seq + row * pitch + col0));
+                v[i] = *reinterpret_cast<const uint4*>(seq + row * pitch + col0);  // global or shared
             else
                 v[i] = make_uint4(0x41414141u, 0x41414141u, 0x41414141u, 0x41414141u);
         }
