@@ -82,18 +82,106 @@ struct SearchCfg {
     static constexpr int NT = 128;
 };
 
-// Planes of one group, one sequence: column `col` plane k at base[(col*3+k)*8].
-// Columns outside [0, m) read as N (lo = hi = 0, N = 1).
-__device__ __forceinline__ void load_col(const uint32_t* __restrict__ base, int col, int m,
+// Column loads relative to a per-block base pointer: word (x*3 + k) * 8 of the
+// group's planes, x counted from the block's first column `col0`. CHECK: the
+// block touches columns outside [0, m), which read as N.
+template <bool CHECK>
+__device__ __forceinline__ void load_rel(const uint32_t* __restrict__ base, int x, int col0, int m,
                                          uint32_t (&v)[3]) {
-    if (static_cast<unsigned>(col) < static_cast<unsigned>(m)) {
-        v[0] = __ldg(base + (col * 3 + 0) * kPackGroups);
-        v[1] = __ldg(base + (col * 3 + 1) * kPackGroups);
-        v[2] = __ldg(base + (col * 3 + 2) * kPackGroups);
+    if (!CHECK || static_cast<unsigned>(col0 + x) < static_cast<unsigned>(m)) {
+        v[0] = __ldg(base + (x * 3 + 0) * kPackGroups);
+        v[1] = __ldg(base + (x * 3 + 1) * kPackGroups);
+        v[2] = __ldg(base + (x * 3 + 2) * kPackGroups);
     } else {
         v[0] = 0u;
         v[1] = 0u;
         v[2] = ~0u;
+    }
+}
+
+// Best candidate of each window of one block (windows j0 .. j0+B-1).
+// tcol0/pcol0: first text / pattern column the block reads; tbase/pbase point
+// at those columns (pointers may be out of range when CHECK masks the load).
+template <int E, bool CHECK>
+__device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase, int tcol0,
+                                             const uint32_t* __restrict__ pbase, int pcol0, int m,
+                                             uint32_t (*Dc)[3], Cand4 (&best)[SearchCfg<E>::B]) {
+    constexpr int B = SearchCfg<E>::B;
+    if constexpr (SearchCfg<E>::CARRY) {
+        // new D columns tcol0 .. tcol0+B-1; pattern column = that + d, pcol0 = tcol0 - E
+        uint32_t T[B][3];
+#pragma unroll
+        for (int b = 0; b < B; ++b) load_rel<CHECK>(tbase, b, tcol0, m, T[b]);
+        uint32_t P[B][3];
+#pragma unroll
+        for (int di = 0; di <= 2 * E; ++di) {
+            if (di == 0) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) load_rel<CHECK>(pbase, b, pcol0, m, P[b]);
+            } else {
+#pragma unroll
+                for (int b = 0; b < B - 1; ++b) {
+                    P[b][0] = P[b + 1][0];
+                    P[b][1] = P[b + 1][1];
+                    P[b][2] = P[b + 1][2];
+                }
+                load_rel<CHECK>(pbase, B - 1 + di, pcol0, m, P[B - 1]);
+            }
+            uint32_t s[B + 3];
+            s[0] = Dc[di][0];
+            s[1] = Dc[di][1];
+            s[2] = Dc[di][2];
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+                s[3 + b] = (P[b][0] ^ T[b][0]) | (P[b][1] ^ T[b][1]) | P[b][2] | T[b][2];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                Cand4 cd;
+                make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
+                if (di == 0)
+                    best[b] = cd;
+                else
+                    update_best4(cd, best[b]);
+            }
+            Dc[di][0] = s[B];
+            Dc[di][1] = s[B + 1];
+            Dc[di][2] = s[B + 2];
+        }
+    } else {
+        // D over columns tcol0 .. tcol0+B+2 rebuilt per block, pcol0 = tcol0 - E.
+        constexpr int X = B + 3;
+        uint32_t T[X][3];
+#pragma unroll
+        for (int x = 0; x < X; ++x) load_rel<CHECK>(tbase, x, tcol0, m, T[x]);
+        uint32_t P[X][3];
+#pragma unroll
+        for (int di = 0; di <= 2 * E; ++di) {
+            if (di == 0) {
+#pragma unroll
+                for (int x = 0; x < X; ++x) load_rel<CHECK>(pbase, x, pcol0, m, P[x]);
+            } else {
+#pragma unroll
+                for (int x = 0; x < X - 1; ++x) {
+                    P[x][0] = P[x + 1][0];
+                    P[x][1] = P[x + 1][1];
+                    P[x][2] = P[x + 1][2];
+                }
+                load_rel<CHECK>(pbase, X - 1 + di, pcol0, m, P[X - 1]);
+            }
+            uint32_t s[X];
+#pragma unroll
+            for (int x = 0; x < X; ++x)
+                s[x] = (P[x][0] ^ T[x][0]) | (P[x][1] ^ T[x][1]) | P[x][2] | T[x][2];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                Cand4 cd;
+                make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
+                if (di == 0)
+                    best[b] = cd;
+                else
+                    update_best4(cd, best[b]);
+            }
+        }
     }
 }
 
@@ -106,6 +194,7 @@ shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
     constexpr int NT = Cfg::NT, B = Cfg::B;
     constexpr bool CARRY = Cfg::CARRY;
     constexpr int NC = 8;  // counter planes: estimates up to 255 (m <= 255 here)
+    constexpr int COLW = 3 * kPackGroups;  // words per column of one group's planes
     const long long g = static_cast<long long>(blockIdx.x) * NT + threadIdx.x;
     const long long row0 = g * 32;
     if (row0 >= n) return;
@@ -124,87 +213,25 @@ shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
 #pragma unroll
     for (int i = 0; i < NC; ++i) cnt[i] = 0u;
 
+    // Block blk covers windows j0 = blk*B-3 .. j0+B-1. It reads text columns
+    // [tcol0, tcol0 + TW) and pattern columns [tcol0 - E, tcol0 + TW + E).
+    constexpr int TOFF = CARRY ? 3 : 0;   // tcol0 = j0 + TOFF
+    constexpr int TW = CARRY ? B : B + 3;
     const int NB = (m + 3 + B - 1) / B;  // blocks: windows must reach m-1
 #pragma unroll 1
     for (int blk = 0; blk < NB; ++blk) {
-        const int j0 = blk * B - 3;  // first window of the block
+        const int j0 = blk * B - 3;
+        const int tcol0 = j0 + TOFF;
+        const int pcol0 = tcol0 - E;
+        const bool interior = tcol0 >= 0 && pcol0 >= 0 && tcol0 + TW + E <= m;
         Cand4 best[B];
-        if constexpr (CARRY) {
-            // new D columns j0+3 .. j0+3+B-1; pattern column = that + d
-            uint32_t T[B][3];
-#pragma unroll
-            for (int b = 0; b < B; ++b) load_col(tb, j0 + 3 + b, m, T[b]);
-            uint32_t P[B][3];
-#pragma unroll
-            for (int di = 0; di <= 2 * E; ++di) {
-                if (di == 0) {
-#pragma unroll
-                    for (int b = 0; b < B; ++b) load_col(pb, j0 + 3 + b - E, m, P[b]);
-                } else {
-#pragma unroll
-                    for (int b = 0; b < B - 1; ++b) {
-                        P[b][0] = P[b + 1][0];
-                        P[b][1] = P[b + 1][1];
-                        P[b][2] = P[b + 1][2];
-                    }
-                    load_col(pb, j0 + 3 + B - 1 - E + di, m, P[B - 1]);
-                }
-                uint32_t s[B + 3];
-                s[0] = Dc[CARRY ? di : 0][0];
-                s[1] = Dc[CARRY ? di : 0][1];
-                s[2] = Dc[CARRY ? di : 0][2];
-#pragma unroll
-                for (int b = 0; b < B; ++b)
-                    s[3 + b] = (P[b][0] ^ T[b][0]) | (P[b][1] ^ T[b][1]) | P[b][2] | T[b][2];
-#pragma unroll
-                for (int b = 0; b < B; ++b) {
-                    Cand4 cd;
-                    make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
-                    if (di == 0)
-                        best[b] = cd;
-                    else
-                        update_best4(cd, best[b]);
-                }
-                Dc[CARRY ? di : 0][0] = s[B];
-                Dc[CARRY ? di : 0][1] = s[B + 1];
-                Dc[CARRY ? di : 0][2] = s[B + 2];
-            }
-        } else {
-            // D over columns j0 .. j0+B+2 rebuilt per block.
-            constexpr int X = B + 3;
-            uint32_t T[X][3];
-#pragma unroll
-            for (int x = 0; x < X; ++x) load_col(tb, j0 + x, m, T[x]);
-            uint32_t P[X][3];
-#pragma unroll
-            for (int di = 0; di <= 2 * E; ++di) {
-                if (di == 0) {
-#pragma unroll
-                    for (int x = 0; x < X; ++x) load_col(pb, j0 + x - E, m, P[x]);
-                } else {
-#pragma unroll
-                    for (int x = 0; x < X - 1; ++x) {
-                        P[x][0] = P[x + 1][0];
-                        P[x][1] = P[x + 1][1];
-                        P[x][2] = P[x + 1][2];
-                    }
-                    load_col(pb, j0 + X - 1 - E + di, m, P[X - 1]);
-                }
-                uint32_t s[X];
-#pragma unroll
-                for (int x = 0; x < X; ++x)
-                    s[x] = (P[x][0] ^ T[x][0]) | (P[x][1] ^ T[x][1]) | P[x][2] | T[x][2];
-#pragma unroll
-                for (int b = 0; b < B; ++b) {
-                    Cand4 cd;
-                    make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
-                    if (di == 0)
-                        best[b] = cd;
-                    else
-                        update_best4(cd, best[b]);
-                }
-            }
-        }
+        // pointers may point outside the group's planes; CHECK masks those loads
+        const uint32_t* tbase = tb + static_cast<long long>(tcol0) * COLW;
+        const uint32_t* pbase = pb + static_cast<long long>(pcol0) * COLW;
+        if (interior)
+            search_block<E, false>(tbase, tcol0, pbase, pcol0, m, Dc, best);
+        else
+            search_block<E, true>(tbase, tcol0, pbase, pcol0, m, Dc, best);
         // commit chain over the block's windows, in column order
         uint32_t outs[B];
 #pragma unroll

@@ -46,60 +46,79 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
-// Bytes of dynamic shared memory for one pair block.
-size_t tile_smem(size_t pitch, int m) {
-    return 2 * size_t(kPackPairs) * pitch + size_t(2) * plane_cols(m) * 3 * kPackGroups * 4;
+// Shared-memory image of one tile: for each (sequence, group) the group's 32
+// records, contiguous (one bulk copy each). Consecutive groups are offset by
+// an extra 16 bytes and the pattern half by 64, so the 8 lanes of a
+// quarter-warp (2 sequences x 4 groups reading the same row/column offset) hit
+// 8 distinct 16-byte bank groups in their LDS.128.
+__host__ __device__ inline size_t group_stride(size_t pitch) { return 32 * pitch + 16; }
+__host__ __device__ inline size_t seq_stride(size_t pitch, int groups) {
+    return groups * group_stride(pitch) + 64;
 }
+size_t tile_smem(size_t pitch, int groups) { return 2 * seq_stride(pitch, groups) + 128; }
+int tile_groups(size_t pitch) { return pitch <= 128 ? 8 : 4; }
 
-// One CTA per pair block: TMA the two record tiles into shared memory, gather
-// 16-column x 32-pair tiles into planes (validating every byte), stage the
-// block's planes in shared memory and write them out contiguously.
+// One CTA per tile of GROUPS x 32 pairs: bulk-copy each group's records into
+// shared memory (TMA, completion on one mbarrier), gather 16-column x 32-pair
+// tiles into planes (validating every byte) and store them straight to the
+// planes array (8 lanes of a warp fill one 32-byte sector per column/plane).
+template <int GROUPS>
 __global__ void __launch_bounds__(kPackNT)
 pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
                  size_t pitch, long long n, int m, uint32_t* __restrict__ planes,
                  uint32_t* __restrict__ err_flag) {
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ __align__(8) uint64_t bar;
-    const long long blk = blockIdx.x;
+    const long long g0 = static_cast<long long>(blockIdx.x) * GROUPS;  // first group
+    const long long row0 = g0 * 32;
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
-    const long long row0 = blk * kPackPairs;
-    const int rows = static_cast<int>(n - row0 < kPackPairs ? n - row0 : kPackPairs);
+    const int rows = static_cast<int>(n - row0 < 32 * GROUPS ? n - row0 : 32 * GROUPS);
     const int mc = plane_cols(m);
-    uint8_t* srec0 = sm;
-    uint8_t* srec1 = sm + size_t(kPackPairs) * pitch;
-    uint32_t* sout = reinterpret_cast<uint32_t*>(sm + 2 * size_t(kPackPairs) * pitch);
-    const uint32_t bytes = static_cast<uint32_t>(rows * pitch);
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
-    __syncthreads();
+    const size_t gs = group_stride(pitch), ss = seq_stride(pitch, GROUPS);
+    auto rec = [&](int sq, int g) { return sm + sq * ss + g * gs; };
     if (threadIdx.x == 0) {
-        mbar_expect_tx(&bar, 2 * bytes);
-        bulk_g2s(srec0, text + row0 * pitch, bytes, &bar);
-        bulk_g2s(srec1, pattern + row0 * pitch, bytes, &bar);
+        mbar_init(&bar, 1);
+        mbar_expect_tx(&bar, static_cast<uint32_t>(2 * rows * pitch));
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * GROUPS) {
+        const int sq = threadIdx.x / GROUPS, g = threadIdx.x % GROUPS;
+        const int r = rows - 32 * g;
+        if (r > 0) {
+            const uint8_t* src = (sq == 0 ? text : pattern) + (row0 + 32 * g) * pitch;
+            bulk_g2s(rec(sq, g), src, static_cast<uint32_t>((r < 32 ? r : 32) * pitch), &bar);
+        }
     }
     mbar_wait(&bar, 0);
-
-    const int C = mc / CH;
-    const int items = 2 * kPackGroups * C;
-    uint32_t err = 0u;
-    for (int it = threadIdx.x; it < items; it += kPackNT) {
-        const int c = it % C;
-        const int g = (it / C) % kPackGroups;
-        const int s = it / (C * kPackGroups);
-        const uint8_t* src = (s == 0 ? srec0 : srec1) + size_t(32 * g) * pitch;
-        uint32_t* dst = sout + (size_t(s) * mc + c * CH) * 3 * kPackGroups + g;
-        const int grows = rows - 32 * g;  // valid rows of this group (may be <= 0)
-        err |= produce_chunk(src, pitch, 0, grows, c, m, dst, kPackGroups);
-    }
-    __syncthreads();
-    if (planes) {
-        // each sequence's block of planes is contiguous in global memory
-        const int words = mc * 3 * kPackGroups;  // per sequence, multiple of 4
-        for (int s = 0; s < 2; ++s) {
-            const uint4* from = reinterpret_cast<const uint4*>(sout + size_t(s) * words);
-            uint4* to = reinterpret_cast<uint4*>(planes + plane_index(s, blk * kPackGroups, 0, 0,
-                                                                      nblocks, mc));
-            for (int i = threadIdx.x; i < words / 4; i += kPackNT) to[i] = from[i];
+    if (rows < 32 * GROUPS) {
+        // last tile: rows past n read as 'A' (valid; their results are masked)
+        const int per_seq = (32 * GROUPS - rows) * static_cast<int>(pitch) / 16;
+        const uint4 a4 = make_uint4(0x41414141u, 0x41414141u, 0x41414141u, 0x41414141u);
+        for (int i = threadIdx.x; i < 2 * per_seq; i += kPackNT) {
+            const int sq = i / per_seq;
+            const int byte = rows * static_cast<int>(pitch) + (i % per_seq) * 16;
+            const int g = byte / (32 * static_cast<int>(pitch));
+            *reinterpret_cast<uint4*>(rec(sq, g) + (byte - g * 32 * static_cast<int>(pitch))) = a4;
         }
+        __syncthreads();
+    }
+    // Items are (chunk, group, sequence) tiles of 32 pairs x 16 columns, the
+    // sequence fastest. Full chunks come first and the one chunk straddling m
+    // (if any) last, so no warp mixes the two gather variants.
+    const int C = mc / CH;
+    const int Cfull = m / CH;  // chunks entirely inside [0, m)
+    uint32_t err = 0u;
+    uint32_t sink[CH * 3];
+    for (int it = threadIdx.x; it < 2 * GROUPS * C; it += kPackNT) {
+        const int c = it / (2 * GROUPS);
+        const int g = (it / 2) % GROUPS;
+        const int sq = it % 2;
+        uint32_t* dst = planes ? planes + plane_index(sq, g0 + g, c * CH, 0, nblocks, mc) : sink;
+        const int stride = planes ? kPackGroups : 1;
+        if (c < Cfull)
+            err |= gather_chunk<false, false>(rec(sq, g), pitch, 0, 32, c * CH, m, dst, stride);
+        else
+            err |= gather_chunk<true, false>(rec(sq, g), pitch, 0, 32, c * CH, m, dst, stride);
     }
     if (err) atomicOr(err_flag, 1u);
 }
@@ -132,21 +151,30 @@ pack_direct_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__
 cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
                         int m, uint32_t* planes, uint32_t* err_flag, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
-    const size_t smem = tile_smem(pitch, m);
-    if (smem <= 200 * 1024) {
-        static size_t attr = 0;  // largest dynamic smem configured so far (idempotent)
-        if (smem > attr) {
-            cudaError_t st = cudaFuncSetAttribute(pack_tile_kernel,
+    const int groups = tile_groups(pitch);
+    const size_t smem = tile_smem(pitch, groups);
+    const long long ngroups = (n + 31) / 32;
+    if (smem <= 110 * 1024) {
+        static bool attr = false;  // idempotent
+        if (!attr) {
+            cudaError_t st = cudaFuncSetAttribute(pack_tile_kernel<8>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  static_cast<int>(200 * 1024));
+                                                  110 * 1024);
+            if (st == cudaSuccess)
+                st = cudaFuncSetAttribute(pack_tile_kernel<4>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
             if (st != cudaSuccess) return st;
-            attr = 200 * 1024;
+            attr = true;
         }
-        const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
-        pack_tile_kernel<<<static_cast<unsigned>(nblocks), kPackNT, smem, s>>>(text, pattern, pitch,
-                                                                              n, m, planes, err_flag);
+        const unsigned grid = static_cast<unsigned>((ngroups + groups - 1) / groups);
+        if (groups == 8)
+            pack_tile_kernel<8><<<grid, kPackNT, smem, s>>>(text, pattern, pitch, n, m, planes,
+                                                            err_flag);
+        else
+            pack_tile_kernel<4><<<grid, kPackNT, smem, s>>>(text, pattern, pitch, n, m, planes,
+                                                            err_flag);
     } else {
-        const long long items = 2 * ((n + 31) / 32) * (plane_cols(m) / CH);
+        const long long items = 2 * ngroups * (plane_cols(m) / CH);
         pack_direct_kernel<<<static_cast<unsigned>((items + kPackNT - 1) / kPackNT), kPackNT, 0,
                              s>>>(text, pattern, pitch, n, m, planes, err_flag);
     }

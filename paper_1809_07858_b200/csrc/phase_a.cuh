@@ -41,7 +41,7 @@ __host__ __device__ constexpr uint32_t crotl(uint32_t x, int s) {
 // dst[(col*3 + k) * dstride], k = 0 lo, 1 hi, 2 N. Returns nonzero on any
 // illegal byte. EDGE: the chunk straddles m (bytes at columns >= m are
 // ignored and their planes forced to N).
-template <bool EDGE>
+template <bool EDGE, bool CHECK_ROWS = true>
 __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq, size_t pitch,
                                                  long long row0, long long n, int col0, int m,
                                                  uint32_t* __restrict__ dst, int dstride) {
@@ -72,7 +72,7 @@ __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const long long row = row0 + 8 * g8 + i;
-            if (row < n)
+            if (!CHECK_ROWS || row < n)
                 v[i] = *reinterpret_cast<const uint4*>(seq + row * pitch + col0);  // global or shared
             else
                 v[i] = make_uint4(0x41414141u, 0x41414141u, 0x41414141u, 0x41414141u);
@@ -143,6 +143,7 @@ __device__ __forceinline__ void fill_oob_chunk(uint32_t* __restrict__ dst, int d
     }
 }
 
+template <bool CHECK_ROWS = true>
 __device__ __forceinline__ uint32_t produce_chunk(const uint8_t* __restrict__ seq, size_t pitch,
                                                   long long row0, long long n, int chunk, int m,
                                                   uint32_t* __restrict__ dst, int dstride) {
@@ -151,8 +152,9 @@ __device__ __forceinline__ uint32_t produce_chunk(const uint8_t* __restrict__ se
         fill_oob_chunk(dst, dstride);
         return 0u;
     }
-    if (col0 + CH <= m) return gather_chunk<false>(seq, pitch, row0, n, col0, m, dst, dstride);
-    return gather_chunk<true>(seq, pitch, row0, n, col0, m, dst, dstride);
+    if (col0 + CH <= m)
+        return gather_chunk<false, CHECK_ROWS>(seq, pitch, row0, n, col0, m, dst, dstride);
+    return gather_chunk<true, CHECK_ROWS>(seq, pitch, row0, n, col0, m, dst, dstride);
 }
 
 }  // namespace sb
