@@ -103,9 +103,9 @@ int pf_shouji_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* patt
 
 /* Same over DEVICE-resident records on the ctx's first device, asynchronous
  * on `stream` (a cudaStream_t; NULL = the legacy default stream) except that an error
- * check forces a stream synchronisation at the end. Records must use
- * pf_device_pitch(m) bytes per row and 16-byte aligned bases (so every row
- * starts 16-byte aligned); bytes in [m, pitch) are ignored. Output pointers
+ * check forces a stream synchronisation at the end. Records need a pitch that
+ * is a multiple of 4 and >= m (pf_device_pitch(m) = round4(m) is the tight
+ * layout) and 16-byte aligned bases; bytes in [m, pitch) are ignored. Output pointers
  * are device pointers (accept_bitmap ceil(n/32) words; estimates/bits as for
  * the host call, may be NULL). */
 int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
@@ -128,7 +128,7 @@ int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint
  * Writes lane-operations per second. */
 int pf_int_peak(pf_ctx* ctx, int op, double* ops_per_second);
 
-/* Row pitch the device entry point expects for length-m records. */
+/* Tight device row pitch for length-m records: round4(m). */
 size_t pf_device_pitch(uint32_t m);
 
 /* Per-pair compatibility entry (a batch of one), reference argument order:

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -49,6 +50,8 @@ struct DeviceState {
     uint8_t* h_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+    sb::Pipeline pipe;           // pack/search overlap for large batches
+    size_t pipe_words[2] = {0, 0};
 };
 
 }  // namespace
@@ -90,6 +93,44 @@ cudaError_t grow(T*& p, size_t& have, size_t need) {
     cudaError_t st = cudaMalloc(&p, n * sizeof(T));
     if (st == cudaSuccess) have = n;
     return st;
+}
+
+// Allocate plane scratch and launch: large fused batches go through the
+// chunked two-stream pipeline, everything else through a single pack+search.
+// Pairs per pipeline chunk (multiple of 256); 0 disables the pipeline.
+// PF_PIPELINE_CHUNK overrides the default (experiments / tuning).
+long long pipeline_chunk() {
+    static const long long v = [] {
+        const char* e = std::getenv("PF_PIPELINE_CHUNK");
+        long long c = e ? std::atoll(e) : sb::kPipelineChunk;
+        return c > 0 ? (c + 255) / 256 * 256 : 0;
+    }();
+    return v;
+}
+
+cudaError_t launch_any(DeviceState& d, sb::FilterArgs a, cudaStream_t s) {
+    const long long chunk = pipeline_chunk();
+    if (sb::pipeline_applies(a, chunk)) {
+        sb::Pipeline& p = d.pipe;
+        cudaError_t st = cudaSuccess;
+        if (!p.side) st = cudaStreamCreateWithFlags(&p.side, cudaStreamNonBlocking);
+        cudaEvent_t* evs[] = {&p.start, &p.done, &p.packed[0], &p.packed[1], &p.searched[0],
+                              &p.searched[1]};
+        for (cudaEvent_t* e : evs)
+            if (st == cudaSuccess && !*e) st = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+        const size_t need = sb::planes_scratch_words(chunk, a.m);
+        for (int b = 0; b < 2 && st == cudaSuccess; ++b) st = grow(p.planes[b], d.pipe_words[b], need);
+        if (st != cudaSuccess) return st;
+        p.planes_words = std::min(d.pipe_words[0], d.pipe_words[1]);
+        p.chunk = chunk;
+        return sb::launch_filter_pipelined(a, p, s);
+    }
+    cudaError_t st = grow(d.d_scratch, d.scratch_words,
+                          sb::planes_scratch_words(a.n, a.m));
+    if (st != cudaSuccess) return st;
+    a.planes = d.d_scratch;
+    a.planes_words = d.scratch_words;
+    return sb::launch_filter(a, s);
 }
 
 bool is_pinned(const void* p) {
@@ -142,7 +183,10 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     const size_t n = p1 - p0;
     if (n == 0) return;
     if (cudaSetDevice(d.device) != cudaSuccess) return fail(PF_ERR_NO_DEVICE);
-    const size_t pitch = pf_device_pitch(m);
+    // Pinned records whose stride is a multiple of 4 are used in place (one DMA
+    // per sequence); anything else is re-pitched on the device to round4(m).
+    const bool pinned = is_pinned(text) && is_pinned(pattern);
+    const size_t pitch = (pinned && stride % 4 == 0) ? stride : pf_device_pitch(m);
     auto cu = [&](cudaError_t ce, const char* what) {
         if (ce == cudaSuccess) return true;
         set_err(err, ce == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA, what, ce);
@@ -160,10 +204,6 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         if (!cu(grow(d.d_outplanes, d.outplanes_words, size_t(m) * ngroups), "alloc tally planes"))
             return;
     }
-    if (e < m && width >= 3 && width <= 8) {
-        const size_t need = sb::planes_scratch_words(static_cast<long long>(n), static_cast<int>(m));
-        if (!cu(grow(d.d_scratch, d.scratch_words, need), "alloc planes")) return;
-    }
     if (!d.d_flag) {
         if (!cu(cudaMalloc(&d.d_flag, sizeof(uint32_t)), "alloc flag")) return;
         if (!cu(cudaMalloc(&d.d_key, sizeof(unsigned long long)), "alloc key")) return;
@@ -178,7 +218,6 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     // DMA of chunk i).
     const uint8_t* tsrc = text + p0 * stride;
     const uint8_t* psrc = pattern + p0 * stride;
-    const bool pinned = is_pinned(text) && is_pinned(pattern);
     if (pinned && stride == pitch) {
         const size_t bytes = (n - 1) * pitch + m;
         if (!cu(cudaMemcpyAsync(d.d_text, tsrc, bytes, cudaMemcpyHostToDevice, d.stream), "H2D text"))
@@ -264,7 +303,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     if (short_circuit || bad_width) {
         if (!cu(sb::launch_validate(a, d.stream), "validate")) return;
     } else {
-        if (!cu(sb::launch_filter(a, d.stream), "filter kernel")) return;
+        if (!cu(launch_any(d, a, d.stream), "filter kernel")) return;
     }
     uint32_t flag = 0;
     if (!cu(cudaMemcpyAsync(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, d.stream),
@@ -341,7 +380,7 @@ int pf_device_count(void) {
     return n;
 }
 
-size_t pf_device_pitch(uint32_t m) { return round_up(std::max<uint32_t>(m, 1), 16); }
+size_t pf_device_pitch(uint32_t m) { return round_up(std::max<uint32_t>(m, 1), 4); }
 
 uint64_t pf_launch_count(void) { return sb::launch_count(); }
 
@@ -397,6 +436,13 @@ void pf_ctx_destroy(pf_ctx* ctx) {
         cudaFree(d.d_flag);
         cudaFree(d.d_key);
         cudaFree(d.d_stage);
+        cudaFree(d.pipe.planes[0]);
+        cudaFree(d.pipe.planes[1]);
+        cudaEvent_t evs[] = {d.pipe.start, d.pipe.done, d.pipe.packed[0], d.pipe.packed[1],
+                             d.pipe.searched[0], d.pipe.searched[1]};
+        for (cudaEvent_t e : evs)
+            if (e) cudaEventDestroy(e);
+        if (d.pipe.side) cudaStreamDestroy(d.pipe.side);
         for (int b = 0; b < 2; ++b) {
             if (d.h_stage[b]) cudaFreeHost(d.h_stage[b]);
             if (d.stage_ev[b]) cudaEventDestroy(d.stage_ev[b]);
@@ -470,11 +516,11 @@ int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
         set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
         return PF_ERR_EMPTY_SEQUENCE;
     }
-    if (pitch % 16 != 0 || pitch < pf_device_pitch(m) ||
+    if (pitch % 4 != 0 || pitch < m ||
         (reinterpret_cast<uintptr_t>(d_text) | reinterpret_cast<uintptr_t>(d_pattern)) % 16 != 0 ||
         m >= (1u << 24)) {
         set_err(err, PF_ERR_INVALID_PARAMETERS,
-                "device records need 16-byte aligned bases and pitch % 16 == 0, pitch >= round16(m)");
+                "device records need 16-byte aligned bases and pitch % 4 == 0, pitch >= m");
         return PF_ERR_INVALID_PARAMETERS;
     }
     std::lock_guard<std::mutex> lock(ctx->mu);
@@ -486,9 +532,6 @@ int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
         PF_CUDA(cudaMalloc(&d.d_flag, sizeof(uint32_t)));
         PF_CUDA(cudaMalloc(&d.d_key, sizeof(unsigned long long)));
     }
-    if (e < m && width >= 3 && width <= 8)
-        PF_CUDA(grow(d.d_scratch, d.scratch_words,
-                     sb::planes_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
     if (d_bits) PF_CUDA(grow(d.d_outplanes, d.outplanes_words, size_t(m) * ngroups));
     PF_CUDA(cudaMemsetAsync(d.d_flag, 0, sizeof(uint32_t), s));
     sb::FilterArgs a{};
@@ -510,7 +553,7 @@ int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
     if (short_circuit || bad_width)
         PF_CUDA(sb::launch_validate(a, s));
     else
-        PF_CUDA(sb::launch_filter(a, s));
+        PF_CUDA(launch_any(d, a, s));
     uint32_t flag = 0;
     PF_CUDA(cudaMemcpyAsync(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
     PF_CUDA(cudaStreamSynchronize(s));
@@ -544,15 +587,13 @@ int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint
     if (n == 0) return PF_OK;
     if (!d_text || !d_pattern || !d_accept_bitmap) return PF_ERR_NULL_ARGUMENT;
     if (m == 0) return PF_ERR_EMPTY_SEQUENCE;
-    if (e >= m || width < 3 || width > 8 || pitch % 16 != 0 || pitch < pf_device_pitch(m) ||
+    if (e >= m || width < 3 || width > 8 || pitch % 4 != 0 || pitch < m ||
         (reinterpret_cast<uintptr_t>(d_text) | reinterpret_cast<uintptr_t>(d_pattern)) % 16 != 0)
         return PF_ERR_INVALID_PARAMETERS;
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceState& d = ctx->devs[0];
     PF_CUDA(cudaSetDevice(d.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    PF_CUDA(grow(d.d_scratch, d.scratch_words,
-                 sb::planes_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
     sb::FilterArgs a{};
     a.text = d_text;
     a.pattern = d_pattern;
@@ -567,7 +608,7 @@ int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint
     a.err_flag = d_err_flag;
     a.planes = d.d_scratch;
     a.planes_words = d.scratch_words;
-    PF_CUDA(sb::launch_filter(a, s));
+    PF_CUDA(launch_any(d, a, s));
     return PF_OK;
 }
 

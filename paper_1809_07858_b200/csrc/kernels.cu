@@ -267,6 +267,42 @@ cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
     return a.m <= 255 ? launch_generic<8>(a, s) : launch_generic<24>(a, s);
 }
 
+bool pipeline_applies(const FilterArgs& a, long long chunk) {
+    return chunk > 0 && a.n > chunk && a.outplanes == nullptr && use_fused(a.width, a.e, a.m);
+}
+
+cudaError_t launch_filter_pipelined(const FilterArgs& a, const Pipeline& p, cudaStream_t s) {
+    const long long chunk = p.chunk;
+    if (chunk % 256 != 0 || p.planes_words < plane_words(chunk, a.m)) return cudaErrorInvalidValue;
+    cudaError_t st = cudaEventRecord(p.start, s);
+    if (st == cudaSuccess) st = cudaStreamWaitEvent(p.side, p.start, 0);
+    const long long nchunks = (a.n + chunk - 1) / chunk;
+    for (long long i = 0; i < nchunks && st == cudaSuccess; ++i) {
+        const int buf = static_cast<int>(i & 1);
+        const long long lo = i * chunk;
+        const long long cn = (a.n - lo < chunk) ? a.n - lo : chunk;
+        // buffer reuse: the search of chunk i-2 must be done reading it
+        if (i >= 2) st = cudaStreamWaitEvent(s, p.searched[buf], 0);
+        if (st != cudaSuccess) break;
+        st = launch_pack(a.text + lo * a.pitch, a.pattern + lo * a.pitch, a.pitch, cn, a.m,
+                         p.planes[buf], a.err_flag, s);
+        if (st == cudaSuccess) st = cudaEventRecord(p.packed[buf], s);
+        if (st == cudaSuccess) st = cudaStreamWaitEvent(p.side, p.packed[buf], 0);
+        if (st != cudaSuccess) break;
+        FilterArgs c = a;
+        c.n = cn;
+        c.planes = p.planes[buf];
+        c.planes_words = p.planes_words;
+        c.accept = a.accept + lo / 32;
+        c.estimates = a.estimates ? a.estimates + lo : nullptr;
+        st = kSearchTable[a.e](c, p.side);
+        if (st == cudaSuccess) st = cudaEventRecord(p.searched[buf], p.side);
+    }
+    if (st == cudaSuccess) st = cudaEventRecord(p.done, p.side);
+    if (st == cudaSuccess) st = cudaStreamWaitEvent(s, p.done, 0);
+    return st;
+}
+
 cudaError_t launch_validate(const FilterArgs& a, cudaStream_t s) {
     return launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, nullptr, a.err_flag, s);
 }

@@ -58,11 +58,24 @@ __host__ __device__ inline size_t seq_stride(size_t pitch, int groups) {
 size_t tile_smem(size_t pitch, int groups) { return 2 * seq_stride(pitch, groups) + 128; }
 int tile_groups(size_t pitch) { return pitch <= 128 ? 8 : 4; }
 
+template <bool EDGE, int ALIGN>
+__device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size_t pitch, int col0,
+                                               int m, uint32_t* dst, int stride) {
+    switch (ncg) {
+        case 1: return gather_chunk<EDGE, false, 1, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
+        case 2: return gather_chunk<EDGE, false, 2, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
+        case 3: return gather_chunk<EDGE, false, 3, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
+        default: return gather_chunk<EDGE, false, 4, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
+    }
+}
+
 // One CTA per tile of GROUPS x 32 pairs: bulk-copy each group's records into
 // shared memory (TMA, completion on one mbarrier), gather 16-column x 32-pair
 // tiles into planes (validating every byte) and store them straight to the
 // planes array (8 lanes of a warp fill one 32-byte sector per column/plane).
-template <int GROUPS>
+// ALIGN = 16 when the record pitch is a multiple of 16 (128-bit shared loads),
+// 4 when it is only a multiple of 4 (tight records, e.g. pitch = m = 100).
+template <int GROUPS, int ALIGN>
 __global__ void __launch_bounds__(kPackNT)
 pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
                  size_t pitch, long long n, int m, uint32_t* __restrict__ planes,
@@ -74,37 +87,53 @@ pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ p
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
     const int rows = static_cast<int>(n - row0 < 32 * GROUPS ? n - row0 : 32 * GROUPS);
     const int mc = plane_cols(m);
+    const int ipitch = static_cast<int>(pitch);
     const size_t gs = group_stride(pitch), ss = seq_stride(pitch, GROUPS);
     auto rec = [&](int sq, int g) { return sm + sq * ss + g * gs; };
+    // bytes of group g moved by TMA (a multiple of 16; a ragged tail is copied below)
+    auto tma_bytes = [&](int g) {
+        const int r = rows - 32 * g;
+        const int b = (r <= 0 ? 0 : (r < 32 ? r : 32)) * ipitch;
+        return b & ~15;
+    };
     if (threadIdx.x == 0) {
+        uint32_t total = 0;
+        for (int g = 0; g < GROUPS; ++g) total += 2u * static_cast<uint32_t>(tma_bytes(g));
         mbar_init(&bar, 1);
-        mbar_expect_tx(&bar, static_cast<uint32_t>(2 * rows * pitch));
+        mbar_expect_tx(&bar, total);
     }
     __syncthreads();
     if (threadIdx.x < 2 * GROUPS) {
         const int sq = threadIdx.x / GROUPS, g = threadIdx.x % GROUPS;
-        const int r = rows - 32 * g;
-        if (r > 0) {
+        const int b = tma_bytes(g);
+        if (b > 0) {
             const uint8_t* src = (sq == 0 ? text : pattern) + (row0 + 32 * g) * pitch;
-            bulk_g2s(rec(sq, g), src, static_cast<uint32_t>((r < 32 ? r : 32) * pitch), &bar);
+            bulk_g2s(rec(sq, g), src, static_cast<uint32_t>(b), &bar);
         }
     }
     mbar_wait(&bar, 0);
     if (rows < 32 * GROUPS) {
-        // last tile: rows past n read as 'A' (valid; their results are masked)
-        const int per_seq = (32 * GROUPS - rows) * static_cast<int>(pitch) / 16;
-        const uint4 a4 = make_uint4(0x41414141u, 0x41414141u, 0x41414141u, 0x41414141u);
+        // last tile: copy the ragged tail of the last group byte-wise, then make
+        // rows past n read as 'A' (valid; their results are masked)
+        const int gl = (rows - 1) / 32;  // group holding the last row
+        const int have = (rows - 32 * gl) * ipitch;
+        const int tb = tma_bytes(gl);
+        for (int i = threadIdx.x; i < 2 * (have - tb); i += kPackNT) {
+            const int sq = i / (have - tb), off = tb + i % (have - tb);
+            rec(sq, gl)[off] = ((sq == 0 ? text : pattern) + (row0 + 32 * gl) * pitch)[off];
+        }
+        const int per_seq = (32 * GROUPS - rows) * ipitch;  // bytes to fill per sequence
         for (int i = threadIdx.x; i < 2 * per_seq; i += kPackNT) {
             const int sq = i / per_seq;
-            const int byte = rows * static_cast<int>(pitch) + (i % per_seq) * 16;
-            const int g = byte / (32 * static_cast<int>(pitch));
-            *reinterpret_cast<uint4*>(rec(sq, g) + (byte - g * 32 * static_cast<int>(pitch))) = a4;
+            const int byte = rows * ipitch + i % per_seq;
+            const int g = byte / (32 * ipitch);
+            rec(sq, g)[byte - g * 32 * ipitch] = 'A';
         }
         __syncthreads();
     }
     // Items are (chunk, group, sequence) tiles of 32 pairs x 16 columns, the
     // sequence fastest. Full chunks come first and the one chunk straddling m
-    // (if any) last, so no warp mixes the two gather variants.
+    // (if any) last, so no warp mixes the gather variants.
     const int C = mc / CH;
     const int Cfull = m / CH;  // chunks entirely inside [0, m)
     uint32_t err = 0u;
@@ -116,9 +145,11 @@ pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ p
         uint32_t* dst = planes ? planes + plane_index(sq, g0 + g, c * CH, 0, nblocks, mc) : sink;
         const int stride = planes ? kPackGroups : 1;
         if (c < Cfull)
-            err |= gather_chunk<false, false>(rec(sq, g), pitch, 0, 32, c * CH, m, dst, stride);
+            err |= gather_chunk<false, false, 4, ALIGN>(rec(sq, g), pitch, 0, 32, c * CH, m, dst,
+                                                         stride);
         else
-            err |= gather_chunk<true, false>(rec(sq, g), pitch, 0, 32, c * CH, m, dst, stride);
+            err |= gather_ncg<true, ALIGN>((m - c * CH + 3) / 4, rec(sq, g), pitch, c * CH, m, dst,
+                                           stride);
     }
     if (err) atomicOr(err_flag, 1u);
 }
@@ -148,38 +179,48 @@ pack_direct_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__
 
 }  // namespace
 
+template <int GROUPS, int ALIGN>
+static cudaError_t launch_tile(const uint8_t* text, const uint8_t* pattern, size_t pitch,
+                               long long n, int m, uint32_t* planes, uint32_t* err_flag,
+                               cudaStream_t s) {
+    static bool attr = false;  // idempotent
+    if (!attr) {
+        cudaError_t st = cudaFuncSetAttribute(pack_tile_kernel<GROUPS, ALIGN>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              110 * 1024);
+        if (st != cudaSuccess) return st;
+        attr = true;
+    }
+    const long long ngroups = (n + 31) / 32;
+    const unsigned grid = static_cast<unsigned>((ngroups + GROUPS - 1) / GROUPS);
+    pack_tile_kernel<GROUPS, ALIGN><<<grid, kPackNT, tile_smem(pitch, GROUPS), s>>>(
+        text, pattern, pitch, n, m, planes, err_flag);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
                         int m, uint32_t* planes, uint32_t* err_flag, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
+    if (pitch % 4 != 0) return cudaErrorInvalidValue;
     const int groups = tile_groups(pitch);
     const size_t smem = tile_smem(pitch, groups);
-    const long long ngroups = (n + 31) / 32;
+    cudaError_t st;
     if (smem <= 110 * 1024) {
-        static bool attr = false;  // idempotent
-        if (!attr) {
-            cudaError_t st = cudaFuncSetAttribute(pack_tile_kernel<8>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  110 * 1024);
-            if (st == cudaSuccess)
-                st = cudaFuncSetAttribute(pack_tile_kernel<4>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
-            if (st != cudaSuccess) return st;
-            attr = true;
-        }
-        const unsigned grid = static_cast<unsigned>((ngroups + groups - 1) / groups);
+        const bool a16 = pitch % 16 == 0;
         if (groups == 8)
-            pack_tile_kernel<8><<<grid, kPackNT, smem, s>>>(text, pattern, pitch, n, m, planes,
-                                                            err_flag);
+            st = a16 ? launch_tile<8, 16>(text, pattern, pitch, n, m, planes, err_flag, s)
+                     : launch_tile<8, 4>(text, pattern, pitch, n, m, planes, err_flag, s);
         else
-            pack_tile_kernel<4><<<grid, kPackNT, smem, s>>>(text, pattern, pitch, n, m, planes,
-                                                            err_flag);
+            st = a16 ? launch_tile<4, 16>(text, pattern, pitch, n, m, planes, err_flag, s)
+                     : launch_tile<4, 4>(text, pattern, pitch, n, m, planes, err_flag, s);
     } else {
-        const long long items = 2 * ngroups * (plane_cols(m) / CH);
+        const long long items = 2 * ((n + 31) / 32) * (plane_cols(m) / CH);
         pack_direct_kernel<<<static_cast<unsigned>((items + kPackNT - 1) / kPackNT), kPackNT, 0,
                              s>>>(text, pattern, pitch, n, m, planes, err_flag);
+        st = cudaGetLastError();
     }
     count_launch();
-    return cudaGetLastError();
+    return st;
 }
 
 }  // namespace sb

@@ -37,26 +37,44 @@ __host__ __device__ constexpr uint32_t crotl(uint32_t x, int s) {
                : (x << (((s % 32) + 32) % 32)) | (x >> (32 - ((s % 32) + 32) % 32));
 }
 
-// Gather columns [col0, col0+16) of rows [row0, row0+32) into plane words.
+// Load 16 bytes of a record row: one 128-bit load when rows are 16-byte
+// aligned, four 32-bit loads when they are only 4-byte aligned (pitch % 4).
+template <int ALIGN>
+__device__ __forceinline__ uint4 load_row16(const uint8_t* p) {
+    if constexpr (ALIGN == 16) {
+        return *reinterpret_cast<const uint4*>(p);
+    } else {
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(p);
+        return make_uint4(q[0], q[1], q[2], q[3]);
+    }
+}
+
+// Gather columns [col0, col0 + 4*NCG) of rows [row0, row0+32) into plane words.
 // dst[(col*3 + k) * dstride], k = 0 lo, 1 hi, 2 N. Returns nonzero on any
 // illegal byte. EDGE: the chunk straddles m (bytes at columns >= m are
-// ignored and their planes forced to N).
-template <bool EDGE, bool CHECK_ROWS = true>
+// ignored; only columns < m are stored). NCG: column groups of 4 processed
+// (fewer than 4 only for the chunk straddling m). ALIGN: row alignment (16/4).
+//
+// Bit k of byte q of row i's word lands at bit 8q+i of the plane-k
+// accumulator by a per-plane shift (left for i >= k, right otherwise) — a
+// multiply or a high multiply, so the shifts issue on the FMA pipe and the
+// ALU pipe only sees the masked ORs.
+template <bool EDGE, bool CHECK_ROWS = true, int NCG = 4, int ALIGN = 16>
 __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq, size_t pitch,
                                                  long long row0, long long n, int col0, int m,
                                                  uint32_t* __restrict__ dst, int dstride) {
-    uint32_t O[4][3][4];  // [column group][plane][column in group] -> column words
+    uint32_t O[NCG][3][4];  // [column group][plane][column in group] -> column words
 #pragma unroll
-    for (int cg = 0; cg < 4; ++cg)
+    for (int cg = 0; cg < NCG; ++cg)
 #pragma unroll
         for (int k = 0; k < 3; ++k)
 #pragma unroll
             for (int q = 0; q < 4; ++q) O[cg][k][q] = 0u;
     uint32_t orr = 0u, andd = ~0u, err = 0u;
-    uint32_t cm[4];
+    uint32_t cm[NCG];
     if (EDGE) {
 #pragma unroll
-        for (int cg = 0; cg < 4; ++cg) {
+        for (int cg = 0; cg < NCG; ++cg) {
             uint32_t mask = 0u;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -73,38 +91,36 @@ __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq
         for (int i = 0; i < 8; ++i) {
             const long long row = row0 + 8 * g8 + i;
             if (!CHECK_ROWS || row < n)
-                v[i] = *reinterpret_cast<const uint4*>(seq + row * pitch + col0);  // global or shared
+                v[i] = load_row16<ALIGN>(seq + row * pitch + col0);  // global or shared
             else
                 v[i] = make_uint4(0x41414141u, 0x41414141u, 0x41414141u, 0x41414141u);
         }
-        uint32_t acc[5][4];
+        uint32_t acc[5][NCG];
 #pragma unroll
         for (int k = 0; k < 5; ++k)
 #pragma unroll
-            for (int cg = 0; cg < 4; ++cg) acc[k][cg] = 0u;
+            for (int cg = 0; cg < NCG; ++cg) acc[k][cg] = 0u;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint32_t wv[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
-            for (int cg = 0; cg < 4; ++cg) {
+            for (int cg = 0; cg < NCG; ++cg) {
                 uint32_t w = wv[cg];
                 if (EDGE) w = (w & cm[cg]) | (0x41414141u & ~cm[cg]);
                 orr |= w;
                 andd &= w;
-                // bit (8q+k) of w lands at (8q+k+i-1) mod 32 for every byte q
-                const uint32_t u = rotl(w, i - 1);
 #pragma unroll
-                for (int k = 0; k < 5; ++k) acc[k][cg] |= u & crotl(0x01010101u, k + i - 1);
+                for (int k = 0; k < 5; ++k) {
+                    const uint32_t u = i >= k ? w * (1u << (i - k)) : __umulhi(w, 1u << (32 - (k - i)));
+                    acc[k][cg] |= u & (0x01010101u << i);
+                }
             }
         }
 #pragma unroll
-        for (int cg = 0; cg < 4; ++cg) {
-            // undo the per-plane offset: bit (8q+i) = bit k of (row 8*g8+i, column 4cg+q)
-            const uint32_t p0 = rotl(acc[0][cg], 1);
-            const uint32_t p1 = acc[1][cg];
-            const uint32_t p2 = rotr(acc[2][cg], 1);
-            const uint32_t p3 = rotr(acc[3][cg], 2);
-            const uint32_t p4 = rotr(acc[4][cg], 3);
+        for (int cg = 0; cg < NCG; ++cg) {
+            // bit (8q+i) of acc[k] = bit k of (row 8*g8+i, column 4cg+q)
+            const uint32_t p0 = acc[0][cg], p1 = acc[1][cg], p2 = acc[2][cg];
+            const uint32_t p3 = acc[3][cg], p4 = acc[4][cg];
             const uint32_t g0 = ~p3 & (~p2 | p1);
             const uint32_t gg4 = p2 & ~p1 & ~p3;
             err |= (p0 ^ g0) | (p4 ^ gg4) | (p3 & ~(p2 & p1));
@@ -120,16 +136,14 @@ __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq
     }
     err |= (orr & 0xA0A0A0A0u) | (~andd & 0x40404040u);
 #pragma unroll
-    for (int cg = 0; cg < 4; ++cg)
+    for (int cg = 0; cg < NCG; ++cg)
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
+        for (int q = 0; q < 4; ++q) {
+            const int col = 4 * cg + q;
+            if (EDGE && col0 + col >= m) continue;  // never read: columns >= m are N
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int col = 4 * cg + q;
-                uint32_t val = O[cg][k][q];
-                if (EDGE && k == 2 && col0 + col >= m) val = ~0u;
-                dst[(col * 3 + k) * dstride] = val;
-            }
+            for (int k = 0; k < 3; ++k) dst[(col * 3 + k) * dstride] = O[cg][k][q];
+        }
     return err;
 }
 
@@ -143,7 +157,8 @@ __device__ __forceinline__ void fill_oob_chunk(uint32_t* __restrict__ dst, int d
     }
 }
 
-template <bool CHECK_ROWS = true>
+// One chunk straight from global memory (long-record path): rows need only be
+// 4-byte aligned.
 __device__ __forceinline__ uint32_t produce_chunk(const uint8_t* __restrict__ seq, size_t pitch,
                                                   long long row0, long long n, int chunk, int m,
                                                   uint32_t* __restrict__ dst, int dstride) {
@@ -153,8 +168,8 @@ __device__ __forceinline__ uint32_t produce_chunk(const uint8_t* __restrict__ se
         return 0u;
     }
     if (col0 + CH <= m)
-        return gather_chunk<false, CHECK_ROWS>(seq, pitch, row0, n, col0, m, dst, dstride);
-    return gather_chunk<true, CHECK_ROWS>(seq, pitch, row0, n, col0, m, dst, dstride);
+        return gather_chunk<false, true, 4, 4>(seq, pitch, row0, n, col0, m, dst, dstride);
+    return gather_chunk<true, true, 4, 4>(seq, pitch, row0, n, col0, m, dst, dstride);
 }
 
 }  // namespace sb

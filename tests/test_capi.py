@@ -50,9 +50,10 @@ def test_status_strings_and_pitch():
     from paper_1809_07858_b200 import _lib
     assert _lib.lib.pf_status_string(2) == b"illegal character"
     assert _lib.lib.pf_status_string(7) == b"invalid parameters"
-    assert _lib.lib.pf_device_pitch(100) == 112
-    assert _lib.lib.pf_device_pitch(250) == 256
-    assert _lib.lib.pf_device_pitch(16) == 16
+    assert _lib.lib.pf_device_pitch(100) == 100
+    assert _lib.lib.pf_device_pitch(250) == 252
+    assert _lib.lib.pf_device_pitch(150) == 152
+    assert _lib.lib.pf_device_pitch(1) == 4
 
 
 def test_no_device_fails_loudly():

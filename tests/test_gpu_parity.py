@@ -333,3 +333,69 @@ def test_pinned_host_buffers(gpu, oracle):
     a, e, _ = gpu.shouji_filter_batch(tp.numpy(), pp.numpy(), 5, estimates=True)
     a2, e2, _ = oracle.shouji_batch(t, p, 5)
     assert (a == a2).all() and (e == e2).all()
+
+
+# --- large batches: the chunked two-stream pipeline equals one-chunk launches -------
+
+@pytest.mark.parametrize("n", [2 * 1048576 + 1, 5 * 1048576 + 37])
+def test_pipelined_large_batch(gpu, oracle, n):
+    import torch
+    m, e = 100, 5
+    pitch = gpu.device_pitch(m)
+    tt = torch.empty((n, pitch), dtype=torch.uint8, device="cuda")
+    pt = torch.empty((n, pitch), dtype=torch.uint8, device="cuda")
+    gpu.generate_device(1, 99, e, tt.data_ptr(), pt.data_ptr(), pitch, n, m)
+    acc = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    est = torch.zeros(n, dtype=torch.int32, device="cuda")
+    gpu.shouji_filter_device(tt.data_ptr(), pt.data_ptr(), pitch, n, m, e, acc.data_ptr(),
+                             d_estimates=est.data_ptr())
+    # reference: the same pairs in sub-chunk pieces (single pack+search each)
+    step = 1 << 20
+    acc2 = torch.zeros_like(acc)
+    est2 = torch.zeros_like(est)
+    for lo in range(0, n, step):
+        cn = min(step, n - lo)
+        gpu.shouji_filter_device(tt[lo:].data_ptr(), pt[lo:].data_ptr(), pitch, cn, m, e,
+                                 acc2[lo // 32:].data_ptr(), d_estimates=est2[lo:].data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(acc, acc2) and torch.equal(est, est2)
+    # and a slice against the oracle, across a chunk boundary
+    lo = (1 << 21) - 4096
+    t = tt[lo:lo + 8192, :m].cpu().numpy()
+    p = pt[lo:lo + 8192, :m].cpu().numpy()
+    a_ref, e_ref, _ = oracle.shouji_batch(t, p, e)
+    assert (acc[lo // 32:(lo + 8192) // 32].cpu().numpy().view(np.uint32) == a_ref).all()
+    assert (est[lo:lo + 8192].cpu().numpy().view(np.uint32) == e_ref).all()
+
+
+@pytest.mark.parametrize("m,pitch", [(100, 100), (100, 112), (100, 128), (96, 96), (37, 40),
+                                     (150, 152), (250, 252), (250, 256), (33, 36)])
+def test_device_pitches(gpu, oracle, m, pitch):
+    """Device records with any pitch that is a multiple of 4 (tight pitch = round4(m))."""
+    import torch
+    rng = np.random.default_rng(m * 1000 + pitch)
+    n = 3000 + m  # ragged last tile
+    t = np.frombuffer(b"ACGTN", np.uint8)[rng.integers(0, 5, size=(n, m))]
+    p = t.copy()
+    mask = rng.random(p.shape) < 0.08
+    p[mask] = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=int(mask.sum()))]
+    buf_t = np.full((n, pitch), ord("z"), np.uint8)
+    buf_p = np.full((n, pitch), ord("z"), np.uint8)
+    buf_t[:, :m] = t
+    buf_p[:, :m] = p
+    tt = torch.from_numpy(buf_t).cuda()
+    pt = torch.from_numpy(buf_p).cuda()
+    for e in (0, 5, min(m - 1, 17)):
+        acc = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+        est = torch.zeros(n, dtype=torch.int32, device="cuda")
+        gpu.shouji_filter_device(tt.data_ptr(), pt.data_ptr(), pitch, n, m, e, acc.data_ptr(),
+                                 d_estimates=est.data_ptr())
+        a_ref, e_ref, _ = oracle.shouji_batch(t, p, e)
+        assert (acc.cpu().numpy().view(np.uint32) == a_ref).all(), (m, pitch, e)
+        assert (est.cpu().numpy().view(np.uint32) == e_ref).all(), (m, pitch, e)
+    # the host path uses such strides in place when pinned
+    a1, e1, _ = gpu.shouji_filter_batch(torch.from_numpy(buf_t).pin_memory().numpy(),
+                                        torch.from_numpy(buf_p).pin_memory().numpy(), 5, m=m,
+                                        estimates=True)
+    a2, e2, _ = oracle.shouji_batch(t, p, 5)
+    assert (a1 == a2).all() and (e1 == e2).all()
