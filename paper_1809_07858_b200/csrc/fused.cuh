@@ -31,6 +31,7 @@
 #include "bitslice.cuh"
 #include "kernels.cuh"
 #include "pack.cuh"
+#include "pack_tile.cuh"
 #include "phase_a.cuh"
 
 namespace sb {
@@ -85,13 +86,21 @@ struct SearchCfg {
 // Column loads relative to a per-block base pointer: word (x*3 + k) * 8 of the
 // group's planes, x counted from the block's first column `col0`. CHECK: the
 // block touches columns outside [0, m), which read as N.
-template <bool CHECK>
+// NC: planes are read-only for the kernel (separate pack kernel) and may use
+// the non-coherent path; the fused kernel writes them itself and must not.
+template <bool CHECK, bool NC = true>
 __device__ __forceinline__ void load_rel(const uint32_t* __restrict__ base, int x, int col0, int m,
                                          uint32_t (&v)[3]) {
     if (!CHECK || static_cast<unsigned>(col0 + x) < static_cast<unsigned>(m)) {
-        v[0] = __ldg(base + (x * 3 + 0) * kPackGroups);
-        v[1] = __ldg(base + (x * 3 + 1) * kPackGroups);
-        v[2] = __ldg(base + (x * 3 + 2) * kPackGroups);
+        if constexpr (NC) {
+            v[0] = __ldg(base + (x * 3 + 0) * kPackGroups);
+            v[1] = __ldg(base + (x * 3 + 1) * kPackGroups);
+            v[2] = __ldg(base + (x * 3 + 2) * kPackGroups);
+        } else {
+            v[0] = base[(x * 3 + 0) * kPackGroups];
+            v[1] = base[(x * 3 + 1) * kPackGroups];
+            v[2] = base[(x * 3 + 2) * kPackGroups];
+        }
     } else {
         v[0] = 0u;
         v[1] = 0u;
@@ -102,7 +111,7 @@ __device__ __forceinline__ void load_rel(const uint32_t* __restrict__ base, int 
 // Best candidate of each window of one block (windows j0 .. j0+B-1).
 // tcol0/pcol0: first text / pattern column the block reads; tbase/pbase point
 // at those columns (pointers may be out of range when CHECK masks the load).
-template <int E, bool CHECK>
+template <int E, bool CHECK, bool NC>
 __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase, int tcol0,
                                              const uint32_t* __restrict__ pbase, int pcol0, int m,
                                              uint32_t (*Dc)[3], Cand4 (&best)[SearchCfg<E>::B]) {
@@ -111,13 +120,13 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
         // new D columns tcol0 .. tcol0+B-1; pattern column = that + d, pcol0 = tcol0 - E
         uint32_t T[B][3];
 #pragma unroll
-        for (int b = 0; b < B; ++b) load_rel<CHECK>(tbase, b, tcol0, m, T[b]);
+        for (int b = 0; b < B; ++b) load_rel<CHECK, NC>(tbase, b, tcol0, m, T[b]);
         uint32_t P[B][3];
 #pragma unroll
         for (int di = 0; di <= 2 * E; ++di) {
             if (di == 0) {
 #pragma unroll
-                for (int b = 0; b < B; ++b) load_rel<CHECK>(pbase, b, pcol0, m, P[b]);
+                for (int b = 0; b < B; ++b) load_rel<CHECK, NC>(pbase, b, pcol0, m, P[b]);
             } else {
 #pragma unroll
                 for (int b = 0; b < B - 1; ++b) {
@@ -125,7 +134,7 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
                     P[b][1] = P[b + 1][1];
                     P[b][2] = P[b + 1][2];
                 }
-                load_rel<CHECK>(pbase, B - 1 + di, pcol0, m, P[B - 1]);
+                load_rel<CHECK, NC>(pbase, B - 1 + di, pcol0, m, P[B - 1]);
             }
             uint32_t s[B + 3];
             s[0] = Dc[di][0];
@@ -152,13 +161,13 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
         constexpr int X = B + 3;
         uint32_t T[X][3];
 #pragma unroll
-        for (int x = 0; x < X; ++x) load_rel<CHECK>(tbase, x, tcol0, m, T[x]);
+        for (int x = 0; x < X; ++x) load_rel<CHECK, NC>(tbase, x, tcol0, m, T[x]);
         uint32_t P[X][3];
 #pragma unroll
         for (int di = 0; di <= 2 * E; ++di) {
             if (di == 0) {
 #pragma unroll
-                for (int x = 0; x < X; ++x) load_rel<CHECK>(pbase, x, pcol0, m, P[x]);
+                for (int x = 0; x < X; ++x) load_rel<CHECK, NC>(pbase, x, pcol0, m, P[x]);
             } else {
 #pragma unroll
                 for (int x = 0; x < X - 1; ++x) {
@@ -166,7 +175,7 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
                     P[x][1] = P[x + 1][1];
                     P[x][2] = P[x + 1][2];
                 }
-                load_rel<CHECK>(pbase, X - 1 + di, pcol0, m, P[X - 1]);
+                load_rel<CHECK, NC>(pbase, X - 1 + di, pcol0, m, P[X - 1]);
             }
             uint32_t s[X];
 #pragma unroll
@@ -185,17 +194,17 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
     }
 }
 
-template <int E>
-__global__ void __launch_bounds__(SearchCfg<E>::NT)
-shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
-                 uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
-                 uint32_t* __restrict__ outplanes) {
+// The whole Shouji sweep for group g (32 pairs) from its planes.
+template <int E, bool NCLOAD>
+__device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes, long long g,
+                                             long long n, int m, uint32_t* __restrict__ accept,
+                                             uint32_t* __restrict__ estimates,
+                                             uint32_t* __restrict__ outplanes) {
     using Cfg = SearchCfg<E>;
-    constexpr int NT = Cfg::NT, B = Cfg::B;
+    constexpr int B = Cfg::B;
     constexpr bool CARRY = Cfg::CARRY;
     constexpr int NC = 8;  // counter planes: estimates up to 255 (m <= 255 here)
     constexpr int COLW = 3 * kPackGroups;  // words per column of one group's planes
-    const long long g = static_cast<long long>(blockIdx.x) * NT + threadIdx.x;
     const long long row0 = g * 32;
     if (row0 >= n) return;
     const long long ngroups = (n + 31) / 32;
@@ -229,9 +238,9 @@ shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
         const uint32_t* tbase = tb + static_cast<long long>(tcol0) * COLW;
         const uint32_t* pbase = pb + static_cast<long long>(pcol0) * COLW;
         if (interior)
-            search_block<E, false>(tbase, tcol0, pbase, pcol0, m, Dc, best);
+            search_block<E, false, NCLOAD>(tbase, tcol0, pbase, pcol0, m, Dc, best);
         else
-            search_block<E, true>(tbase, tcol0, pbase, pcol0, m, Dc, best);
+            search_block<E, true, NCLOAD>(tbase, tcol0, pbase, pcol0, m, Dc, best);
         // commit chain over the block's windows, in column order
         uint32_t outs[B];
 #pragma unroll
@@ -270,6 +279,47 @@ shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
 }
 
 template <int E>
+__global__ void __launch_bounds__(SearchCfg<E>::NT)
+shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
+                 uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
+                 uint32_t* __restrict__ outplanes) {
+    const long long g = static_cast<long long>(blockIdx.x) * SearchCfg<E>::NT + threadIdx.x;
+    search_group<E, true>(planes, g, n, m, accept, estimates, outplanes);
+}
+
+// Pack + search in one kernel: a CTA packs the planes of its 128 groups
+// (4096 pairs; TMA tiles, pack_tile.cuh) into the planes array, then each
+// thread sweeps one group. Different CTAs on an SM sit in different phases,
+// so the memory-bound packing of one overlaps the integer-bound search of
+// another; the planes a CTA reads back were written moments before (L2).
+constexpr int kFusedNT = 128;
+
+template <int E>
+__global__ void __launch_bounds__(kFusedNT)
+shouji_fused_w4(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern, size_t pitch,
+                long long n, int m, int tile_groups, uint32_t* __restrict__ planes,
+                uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
+                uint32_t* __restrict__ err_flag) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    const long long ngroups = (n + 31) / 32;
+    const long long gbase = static_cast<long long>(blockIdx.x) * kFusedNT;
+    uint32_t err = 0u, parity = 0u;
+    for (int t = 0; t < kFusedNT / tile_groups; ++t) {
+        const long long g0 = gbase + static_cast<long long>(t) * tile_groups;
+        if (g0 >= ngroups) break;
+        err |= pack_one_tile<4, kFusedNT>(sm, &bar, parity, tile_groups, g0, text, pattern, pitch, n,
+                                          m, planes);
+        parity ^= 1u;
+    }
+    if (err) atomicOr(err_flag, 1u);
+    __syncthreads();  // this CTA's planes are written (CTA-scope ordering)
+    search_group<E, false>(planes, gbase + threadIdx.x, n, m, accept, estimates, nullptr);
+}
+
+template <int E>
 cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s) {
     using Cfg = SearchCfg<E>;
     const long long ngroups = (a.n + 31) / 32;
@@ -280,8 +330,28 @@ cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int E>
+cudaError_t launch_fused_e(const FilterArgs& a, cudaStream_t s) {
+    const int groups = tile_groups(a.pitch);
+    const size_t smem = tile_smem(a.pitch, groups);
+    static bool attr = false;  // per instantiation; idempotent
+    if (!attr) {
+        cudaError_t st = cudaFuncSetAttribute(shouji_fused_w4<E>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+        if (st != cudaSuccess) return st;
+        attr = true;
+    }
+    const long long ngroups = (a.n + 31) / 32;
+    const unsigned grid = static_cast<unsigned>((ngroups + kFusedNT - 1) / kFusedNT);
+    shouji_fused_w4<E><<<grid, kFusedNT, smem, s>>>(a.text, a.pattern, a.pitch, a.n, a.m, groups,
+                                                     a.planes, a.accept, a.estimates, a.err_flag);
+    count_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace sb
 
 // Explicit instantiation helper for the fused_e*.cu units.
-#define SB_INSTANTIATE_FUSED(E) \
-    template cudaError_t sb::launch_search_e<E>(const sb::FilterArgs&, cudaStream_t);
+#define SB_INSTANTIATE_FUSED(E)                                                      \
+    template cudaError_t sb::launch_search_e<E>(const sb::FilterArgs&, cudaStream_t); \
+    template cudaError_t sb::launch_fused_e<E>(const sb::FilterArgs&, cudaStream_t);

@@ -33,9 +33,11 @@
 #include "bitslice.cuh"
 #include "kernels.cuh"
 #include "pack.cuh"
+#include "pack_tile.cuh"
 #include "phase_a.cuh"
 
 #include <array>
+#include <cstdlib>
 #include <utility>
 
 namespace sb {
@@ -220,14 +222,32 @@ __global__ void accept_all(long long n, int m, uint32_t* accept, uint32_t* estim
 // parallel: each E is its own fully unrolled kernel).
 template <int E>
 cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s);
+template <int E>
+cudaError_t launch_fused_e(const FilterArgs& a, cudaStream_t s);
 
 using SearchFn = cudaError_t (*)(const FilterArgs&, cudaStream_t);
 template <int... Es>
 static constexpr std::array<SearchFn, sizeof...(Es)> make_search_table(std::integer_sequence<int, Es...>) {
     return {&launch_search_e<Es>...};
 }
+template <int... Es>
+static constexpr std::array<SearchFn, sizeof...(Es)> make_fused_table(std::integer_sequence<int, Es...>) {
+    return {&launch_fused_e<Es>...};
+}
 static constexpr auto kSearchTable =
     make_search_table(std::make_integer_sequence<int, kFusedMaxE + 1>{});
+static constexpr auto kFusedTable =
+    make_fused_table(std::make_integer_sequence<int, kFusedMaxE + 1>{});
+
+// One-kernel pack+search (shouji_fused_w4) only when PF_FUSED=1: measured
+// slower than pack + search on B200 (profiles/r1_notes.md), kept for A/B runs.
+static bool fused_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("PF_FUSED");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
 
 template <int W, int NC>
 static cudaError_t launch_generic_w(const FilterArgs& a, cudaStream_t s) {
@@ -261,6 +281,9 @@ bool use_fused(uint32_t width, uint32_t e, int m) {
 cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
     if (a.n <= 0) return cudaSuccess;
     if (a.planes == nullptr || a.planes_words < plane_words(a.n, a.m)) return cudaErrorInvalidValue;
+    const bool tile_ok = tile_smem(a.pitch, tile_groups(a.pitch)) <= 110 * 1024 && a.pitch % 4 == 0;
+    if (use_fused(a.width, a.e, a.m) && tile_ok && a.outplanes == nullptr && fused_enabled())
+        return kFusedTable[a.e](a, s);
     cudaError_t st = launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, a.planes, a.err_flag, s);
     if (st != cudaSuccess) return st;
     if (use_fused(a.width, a.e, a.m)) return kSearchTable[a.e](a, s);

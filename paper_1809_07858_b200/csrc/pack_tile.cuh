@@ -1,0 +1,153 @@
+// Tile machinery shared by the pack kernel and the fused kernel: TMA bulk
+// copies of 32-record groups into bank-skewed shared memory, completion on an
+// mbarrier, then the in-register gather of phase_a.cuh.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pack.cuh"
+#include "phase_a.cuh"
+
+namespace sb {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+// Shared-memory image of one tile: for each (sequence, group) the group's 32
+// records, contiguous (one bulk copy each). Consecutive groups are offset by
+// an extra 16 bytes and the pattern half by 64, so the 8 lanes of a
+// quarter-warp (2 sequences x 4 groups reading the same row/column offset) hit
+// 8 distinct 16-byte bank groups in their LDS.128.
+__host__ __device__ inline size_t group_stride(size_t pitch) { return 32 * pitch + 16; }
+__host__ __device__ inline size_t seq_stride(size_t pitch, int groups) {
+    return groups * group_stride(pitch) + 64;
+}
+inline size_t tile_smem(size_t pitch, int groups) { return 2 * seq_stride(pitch, groups) + 128; }
+inline int tile_groups(size_t pitch) { return pitch <= 128 ? 8 : 4; }
+
+template <bool EDGE, int ALIGN>
+__device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size_t pitch, int col0,
+                                               int m, uint32_t* dst, int stride) {
+    switch (ncg) {
+        case 1: return gather_chunk<EDGE, false, 1, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
+        case 2: return gather_chunk<EDGE, false, 2, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
+        case 3: return gather_chunk<EDGE, false, 3, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
+        default: return gather_chunk<EDGE, false, 4, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
+    }
+}
+
+// Pack one tile of GROUPS x 32 pairs starting at group g0 (all threads of the
+// CTA call it; NT threads). sm: tile_smem() bytes of dynamic shared memory;
+// bar: an initialised mbarrier; parity: its current phase (flipped on return
+// by the caller). Returns nonzero on an illegal byte.
+template <int ALIGN, int NT>
+__device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, uint32_t parity,
+                                                  int GROUPS, long long g0,
+                                                  const uint8_t* __restrict__ text,
+                                                  const uint8_t* __restrict__ pattern, size_t pitch,
+                                                  long long n, int m, uint32_t* __restrict__ planes) {
+    const long long row0 = g0 * 32;
+    const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
+    const int rows = static_cast<int>(n - row0 < 32 * GROUPS ? n - row0 : 32 * GROUPS);
+    const int mc = plane_cols(m);
+    const int ipitch = static_cast<int>(pitch);
+    const size_t gs = group_stride(pitch), ss = seq_stride(pitch, GROUPS);
+    auto rec = [&](int sq, int g) { return sm + sq * ss + g * gs; };
+    // bytes of group g moved by TMA (a multiple of 16; a ragged tail is copied below)
+    auto tma_bytes = [&](int g) {
+        const int r = rows - 32 * g;
+        const int b = (r <= 0 ? 0 : (r < 32 ? r : 32)) * ipitch;
+        return b & ~15;
+    };
+    if (threadIdx.x == 0) {
+        uint32_t total = 0;
+        for (int g = 0; g < GROUPS; ++g) total += 2u * static_cast<uint32_t>(tma_bytes(g));
+        mbar_expect_tx(bar, total);
+    }
+    __syncthreads();  // expect_tx before any complete_tx; previous tile's readers done
+    if (threadIdx.x < 2 * GROUPS) {
+        const int sq = threadIdx.x / GROUPS, g = threadIdx.x % GROUPS;
+        const int b = tma_bytes(g);
+        if (b > 0) {
+            const uint8_t* src = (sq == 0 ? text : pattern) + (row0 + 32 * g) * pitch;
+            bulk_g2s(rec(sq, g), src, static_cast<uint32_t>(b), bar);
+        }
+    }
+    mbar_wait(bar, parity);
+    if (rows < 32 * GROUPS) {
+        // last tile: copy the ragged tail of the last group byte-wise, then make
+        // rows past n read as 'A' (valid; their results are masked)
+        const int gl = (rows - 1) / 32;  // group holding the last row
+        const int have = (rows - 32 * gl) * ipitch;
+        const int tb = tma_bytes(gl);
+        for (int i = threadIdx.x; i < 2 * (have - tb); i += NT) {
+            const int sq = i / (have - tb), off = tb + i % (have - tb);
+            rec(sq, gl)[off] = ((sq == 0 ? text : pattern) + (row0 + 32 * gl) * pitch)[off];
+        }
+        const int per_seq = (32 * GROUPS - rows) * ipitch;  // bytes to fill per sequence
+        for (int i = threadIdx.x; i < 2 * per_seq; i += NT) {
+            const int sq = i / per_seq;
+            const int byte = rows * ipitch + i % per_seq;
+            const int g = byte / (32 * ipitch);
+            rec(sq, g)[byte - g * 32 * ipitch] = 'A';
+        }
+        __syncthreads();
+    }
+    // Items are (chunk, group, sequence) tiles of 32 pairs x 16 columns, the
+    // sequence fastest. Full chunks come first and the one chunk straddling m
+    // (if any) last, so no warp mixes the gather variants.
+    const int C = mc / CH;
+    const int Cfull = m / CH;  // chunks entirely inside [0, m)
+    uint32_t err = 0u;
+    uint32_t sink[CH * 3];
+    for (int it = threadIdx.x; it < 2 * GROUPS * C; it += NT) {
+        const int c = it / (2 * GROUPS);
+        const int g = (it / 2) % GROUPS;
+        const int sq = it % 2;
+        uint32_t* dst = planes ? planes + plane_index(sq, g0 + g, c * CH, 0, nblocks, mc) : sink;
+        const int stride = planes ? kPackGroups : 1;
+        if (c < Cfull)
+            err |= gather_chunk<false, false, 4, ALIGN>(rec(sq, g), pitch, 0, 32, c * CH, m, dst,
+                                                         stride);
+        else
+            err |= gather_ncg<true, ALIGN>((m - c * CH + 3) / 4, rec(sq, g), pitch, c * CH, m, dst,
+                                           stride);
+    }
+    return err;
+}
+
+}  // namespace sb
