@@ -67,6 +67,7 @@ typedef struct pf_error {
     uint64_t position;
     uint32_t byte;
     int32_t cuda_error; /* cudaError_t when status == PF_ERR_CUDA */
+    uint64_t line;      /* 1-based input line for PF_ERR_PARSE / dataset length errors */
     char message[160];
 } pf_error;
 
@@ -131,6 +132,15 @@ int pf_int_peak(pf_ctx* ctx, int op, double* ops_per_second);
 /* Tight device row pitch for length-m records: round4(m). */
 size_t pf_device_pitch(uint32_t m);
 
+/* Exact alignment oracle / verification step on the GPU:
+ * banded_edit_distance(pattern, text, e) (proj/src/edit_distance.cpp:26-70)
+ * for every pair of host records: out[i] = distance if <= e, else -1 (the
+ * reference's std::nullopt). N matches nothing. Same validation and error
+ * reporting as pf_shouji_filter_batch; m <= 1024. */
+int pf_banded_edit_distance_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern,
+                                  size_t stride, size_t n, uint32_t m, uint32_t e, int32_t* out,
+                                  pf_error* err);
+
 /* Per-pair compatibility entry (a batch of one), reference argument order:
  * shouji_filter(pattern, text, e, width). Lengths may differ (->
  * PF_ERR_LENGTH_MISMATCH, checked before the width, shouji.cpp:44-47).
@@ -150,6 +160,35 @@ void pf_host_free(void* p);
  * (kind, seed, param, pair index). */
 int pf_generate_device(pf_ctx* ctx, int kind, uint64_t seed, uint32_t param, uint8_t* d_text,
                        uint8_t* d_pattern, size_t pitch, size_t n, uint32_t m, void* stream);
+
+/* ---- Pair datasets: the caller side of the path (dataset.hpp / dataset.cpp) ----
+ * A dataset holds n equal-length ASCII pairs as fixed-stride records (stride =
+ * m, pinned host memory when available), ready for pf_shouji_filter_batch. */
+typedef struct pf_dataset pf_dataset;
+
+/* load_pairs (proj/src/dataset.cpp:13-44): one TEXT '\t' PATTERN pair per
+ * line. Byte validation runs on the ctx's GPU; errors are the ones the
+ * reference's line-by-line loader throws first: PF_ERR_PARSE with err->line for
+ * a wrong field count, an empty field or an illegal byte (err->position/byte),
+ * PF_ERR_LENGTH_MISMATCH with err->line for unequal lengths, PF_ERR_PARSE line
+ * 1 for an input without pairs. */
+int pf_dataset_load_tsv(pf_ctx* ctx, const char* data, size_t len, const char* source_name,
+                        pf_dataset** out, pf_error* err);
+int pf_dataset_load_tsv_file(pf_ctx* ctx, const char* path, pf_dataset** out, pf_error* err);
+/* generate_pairs({seed, count, length, {lo, hi}}) (dataset.cpp:71-126), byte-identical. */
+int pf_dataset_generate(uint64_t seed, size_t count, uint32_t length, uint32_t lo, uint32_t hi,
+                        pf_dataset** out, pf_error* err);
+/* Copy caller records (stride >= m) into a dataset. */
+int pf_dataset_from_records(const uint8_t* text, const uint8_t* pattern, size_t stride, size_t n,
+                            uint32_t m, const char* source_name, pf_dataset** out);
+size_t pf_dataset_size(const pf_dataset* ds);
+uint32_t pf_dataset_length(const pf_dataset* ds);
+const uint8_t* pf_dataset_text(const pf_dataset* ds);
+const uint8_t* pf_dataset_pattern(const pf_dataset* ds);
+const char* pf_dataset_source(const pf_dataset* ds);
+/* write_pairs (dataset.cpp:53-56); path "-" = stdout. */
+int pf_dataset_write_tsv(const pf_dataset* ds, const char* path);
+void pf_dataset_free(pf_dataset* ds);
 
 /* Number of kernel launches issued by this process so far (all contexts);
  * bench.py reports the delta over its timed region. */

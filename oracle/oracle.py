@@ -143,7 +143,16 @@ class Reference:
                                        C.c_uint, C.POINTER(C.c_int), C.POINTER(C.c_uint32),
                                        C.c_char_p]
         lib.ref_hardware_concurrency.restype = C.c_uint
+        lib.ref_load_pairs_tsv.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t),
+                                           C.POINTER(C.c_size_t), C.c_char_p, C.c_size_t]
         self.lib = lib
+
+    def load_pairs(self, data: bytes):
+        """load_pairs over bytes -> (status, n, m, message)."""
+        n, m = C.c_size_t(), C.c_size_t()
+        buf = C.create_string_buffer(512)
+        st = self.lib.ref_load_pairs_tsv(data, len(data), C.byref(n), C.byref(m), buf, 512)
+        return st, n.value, m.value, buf.value.decode(errors="replace")
 
     @staticmethod
     def available(path=REF_SO):

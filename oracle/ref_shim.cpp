@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -243,6 +244,25 @@ int ref_shouji_one(const char* pattern, std::size_t pattern_len, const char* tex
         }
         return kOk;
     } catch (...) {
+        return map_exception(std::current_exception(), nullptr);
+    }
+}
+
+// load_pairs (proj/src/dataset.cpp:13-44) over an in-memory TSV; on failure
+// returns the mapped status and copies e.what() into msg.
+int ref_load_pairs_tsv(const char* data, std::size_t len, std::size_t* n, std::size_t* m,
+                       char* msg, std::size_t msglen) {
+    std::istringstream in(std::string(data, len));
+    try {
+        const auto ds = prefilter::load_pairs(in, "<stream>");
+        *n = ds.pairs.size();
+        *m = ds.length;
+        return kOk;
+    } catch (const std::exception& e) {
+        if (msg && msglen) {
+            std::strncpy(msg, e.what(), msglen - 1);
+            msg[msglen - 1] = '\0';
+        }
         return map_exception(std::current_exception(), nullptr);
     }
 }

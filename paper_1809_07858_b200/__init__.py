@@ -36,6 +36,13 @@ from .api import (  # noqa: F401
     int_peak,
     threshold_too_large_error,
     unpack_bitmap,
+    banded_edit_distance,
+    banded_edit_distance_batch,
+    pair_dataset,
+    load_pairs,
+    load_pairs_file,
+    generate_pairs,
+    write_pairs,
 )
 
 __version__ = "0.1.0"

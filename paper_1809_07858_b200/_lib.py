@@ -31,6 +31,9 @@ EXPORTED = [
     "pf_ctx_device_count", "pf_shouji_filter_batch", "pf_shouji_filter_device", "pf_device_pitch",
     "pf_shouji_filter_one", "pf_host_alloc", "pf_host_free", "pf_generate_device", "pf_launch_count",
     "pf_shouji_filter_device_async", "pf_int_peak",
+    "pf_dataset_load_tsv", "pf_dataset_load_tsv_file", "pf_dataset_generate", "pf_dataset_from_records",
+    "pf_dataset_size", "pf_dataset_length", "pf_dataset_text", "pf_dataset_pattern",
+    "pf_dataset_source", "pf_dataset_write_tsv", "pf_dataset_free", "pf_banded_edit_distance_batch",
 ]
 
 
@@ -42,6 +45,7 @@ class PfError(C.Structure):
         ("position", C.c_uint64),
         ("byte", C.c_uint32),
         ("cuda_error", C.c_int32),
+        ("line", C.c_uint64),
         ("message", C.c_char * 160),
     ]
 
@@ -75,6 +79,21 @@ def _bind(lib):
         "pf_shouji_filter_device_async": (C.c_int, [_vp, _vp, _vp, _sz, _sz, _u32, _u32, _u32, _vp,
                                                     _vp, _vp, _vp]),
         "pf_int_peak": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_double)]),
+        "pf_dataset_load_tsv": (C.c_int, [_vp, C.c_char_p, _sz, C.c_char_p, C.POINTER(_vp),
+                                          C.POINTER(PfError)]),
+        "pf_dataset_load_tsv_file": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp), C.POINTER(PfError)]),
+        "pf_dataset_generate": (C.c_int, [C.c_uint64, _sz, _u32, _u32, _u32, C.POINTER(_vp),
+                                          C.POINTER(PfError)]),
+        "pf_dataset_from_records": (C.c_int, [_vp, _vp, _sz, _sz, _u32, C.c_char_p, C.POINTER(_vp)]),
+        "pf_dataset_size": (_sz, [_vp]),
+        "pf_dataset_length": (_u32, [_vp]),
+        "pf_dataset_text": (_vp, [_vp]),
+        "pf_dataset_pattern": (_vp, [_vp]),
+        "pf_dataset_source": (C.c_char_p, [_vp]),
+        "pf_dataset_write_tsv": (C.c_int, [_vp, C.c_char_p]),
+        "pf_dataset_free": (None, [_vp]),
+        "pf_banded_edit_distance_batch": (C.c_int, [_vp, _vp, _vp, _sz, _sz, _u32, _u32, _vp,
+                                                    C.POINTER(PfError)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

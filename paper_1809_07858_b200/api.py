@@ -93,6 +93,10 @@ def _raise(status: int, err: L.PfError | None = None):
         raise illegal_character_error(int(err.position), int(err.byte), int(err.pair), int(err.field))
     if status == L.PF_ERR_LENGTH_MISMATCH:
         raise length_mismatch_error(msg)
+    if status == L.PF_ERR_PARSE:
+        line = int(err.line) if err is not None else 0
+        prefix = f"line {line}: "
+        raise parse_error(line, msg[len(prefix):] if msg.startswith(prefix) else msg)
     if status == L.PF_ERR_THRESHOLD_TOO_LARGE:
         raise threshold_too_large_error(msg)
     if status == L.PF_ERR_OUT_OF_BAND:
@@ -372,3 +376,117 @@ def int_peak(op: str = "lop3", ctx: Context | None = None) -> float:
     out = C.c_double()
     _raise(L.lib.pf_int_peak(ctx.handle, code, C.byref(out)))
     return out.value
+
+
+# ---------------------------------------------------------------------------
+# Exact alignment oracle on the GPU (edit_distance.hpp:13-20)
+# ---------------------------------------------------------------------------
+def banded_edit_distance_batch(text, pattern, e: int, m: int | None = None,
+                               ctx: Context | None = None) -> np.ndarray:
+    """banded_edit_distance(pattern[i], text[i], e) for every pair: int32, -1 = out of band."""
+    ctx = ctx or default_context()
+    text = _as_records(text)
+    pattern = _as_records(pattern)
+    n, stride = text.shape
+    m = stride if m is None else int(m)
+    out = np.zeros(n, np.int32)
+    err = L.PfError()
+    st = L.lib.pf_banded_edit_distance_batch(ctx.handle, text.ctypes.data_as(C.c_void_p),
+                                             pattern.ctypes.data_as(C.c_void_p), stride, n, m,
+                                             int(e), out.ctypes.data_as(C.c_void_p), C.byref(err))
+    _raise(st, err)
+    return out
+
+
+def banded_edit_distance(a: packed_sequence, b: packed_sequence, e: int, ctx: Context | None = None):
+    """Distance if <= e else None (edit_distance.cpp:26-70); lengths must match."""
+    if a.size() != b.size():
+        raise length_mismatch_error(f"length mismatch: {a.size()} vs {b.size()}")
+    d = banded_edit_distance_batch(np.frombuffer(b.ascii(), np.uint8)[None, :],
+                                   np.frombuffer(a.ascii(), np.uint8)[None, :], e, ctx=ctx)[0]
+    return None if d < 0 else int(d)
+
+
+# ---------------------------------------------------------------------------
+# Pair datasets (dataset.hpp:13-58): TSV ingest with GPU validation, generator
+# ---------------------------------------------------------------------------
+class pair_dataset:
+    """n equal-length pairs as fixed-stride ASCII records (pinned host memory)."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+
+    def __len__(self):
+        return int(L.lib.pf_dataset_size(self._h))
+
+    @property
+    def length(self) -> int:
+        return int(L.lib.pf_dataset_length(self._h))
+
+    @property
+    def source(self) -> str:
+        return L.lib.pf_dataset_source(self._h).decode()
+
+    def _view(self, fn):
+        n, m = len(self), self.length
+        ptr = fn(self._h)
+        if not n:
+            return np.zeros((0, m), np.uint8)
+        buf = (C.c_uint8 * (n * m)).from_address(ptr)
+        return np.frombuffer(buf, np.uint8).reshape(n, m)
+
+    def text(self) -> np.ndarray:
+        return self._view(L.lib.pf_dataset_text)
+
+    def pattern(self) -> np.ndarray:
+        return self._view(L.lib.pf_dataset_pattern)
+
+    def filter(self, e: int, width: int = default_window_width, estimates: bool = False,
+               ctx: Context | None = None):
+        return shouji_filter_batch(self.text(), self.pattern(), e, width, estimates=estimates, ctx=ctx)
+
+    def write(self, path: str) -> None:
+        if L.lib.pf_dataset_write_tsv(self._h, path.encode()) != L.PF_OK:
+            raise error(f"cannot open output file: {path}")
+
+    def close(self):
+        if self._h:
+            L.lib.pf_dataset_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def load_pairs(data, source_name: str = "<stream>", ctx: Context | None = None) -> pair_dataset:
+    """load_pairs (dataset.cpp:13-44) over bytes/str; parse_error(line) semantics."""
+    ctx = ctx or default_context()
+    b = data.encode() if isinstance(data, str) else bytes(data)
+    h = C.c_void_p()
+    err = L.PfError()
+    _raise(L.lib.pf_dataset_load_tsv(ctx.handle, b, len(b), source_name.encode(), C.byref(h),
+                                     C.byref(err)), err)
+    return pair_dataset(h)
+
+
+def load_pairs_file(path: str, ctx: Context | None = None) -> pair_dataset:
+    ctx = ctx or default_context()
+    h = C.c_void_p()
+    err = L.PfError()
+    _raise(L.lib.pf_dataset_load_tsv_file(ctx.handle, path.encode(), C.byref(h), C.byref(err)), err)
+    return pair_dataset(h)
+
+
+def generate_pairs(seed: int, count: int, length: int, lo: int, hi: int) -> pair_dataset:
+    """generate_pairs({seed, count, length, {lo, hi}}) — byte-identical to the reference."""
+    h = C.c_void_p()
+    err = L.PfError()
+    _raise(L.lib.pf_dataset_generate(seed, count, length, lo, hi, C.byref(h), C.byref(err)), err)
+    return pair_dataset(h)
+
+
+def write_pairs(ds: pair_dataset, path: str) -> None:
+    ds.write(path)

@@ -18,6 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libshouji_b200.so")
+CLI = os.path.join(PKG, "shouji-b200")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -81,6 +82,14 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    # command-line caller (tools/shouji_cli.cpp), linked against the library
+    cli_src = os.path.join(PKG, "tools", "shouji_cli.cpp")
+    if _stale(CLI, [cli_src, LIB, os.path.join(ROOT, "include", "shouji_b200.h")]):
+        cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I" + os.path.join(ROOT, "include"), cli_src,
+               "-o", CLI, "-L" + PKG, "-lshouji_b200", "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
     if verbose:
         for lg in logs:
             sys.stderr.write(lg)

@@ -173,10 +173,12 @@ struct ShardResult {
     pf_error err{};
 };
 
-// Filter pairs [p0, p1) of host records on one device.
+// Filter pairs [p0, p1) of host records on one device. With `dist` set the
+// shard computes exact banded edit distances instead (validation, then the
+// Myers kernel; accept/estimates/bits unused).
 void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern, size_t stride,
                     size_t p0, size_t p1, uint32_t m, uint32_t e, uint32_t width,
-                    uint32_t* accept_bitmap, uint32_t* estimates, uint64_t* bits,
+                    uint32_t* accept_bitmap, uint32_t* estimates, uint64_t* bits, int32_t* dist,
                     ShardResult* res) {
     pf_error* err = &res->err;
     auto fail = [&](int st) { res->status = st; };
@@ -197,7 +199,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     if (!cu(grow(d.d_pattern, d.in_pattern_bytes, n * pitch), "alloc pattern")) return;
     const size_t ngroups = (n + 31) / 32;
     if (!cu(grow(d.d_accept, d.accept_words, ngroups), "alloc accept")) return;
-    if (estimates && !cu(grow(d.d_est, d.est_n, n), "alloc estimates")) return;
+    if ((estimates || dist) && !cu(grow(d.d_est, d.est_n, n), "alloc estimates")) return;
     const size_t wpp = (m + 63) / 64;
     if (bits) {
         if (!cu(grow(d.d_bits, d.bits_words, n * wpp), "alloc bits")) return;
@@ -299,8 +301,8 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     a.planes = d.d_scratch;
     a.planes_words = d.scratch_words;
     const bool short_circuit = e >= m;
-    const bool bad_width = width < 3 || width > 8;
-    if (short_circuit || bad_width) {
+    const bool bad_width = !dist && (width < 3 || width > 8);
+    if (short_circuit || bad_width || dist) {
         if (!cu(sb::launch_validate(a, d.stream), "validate")) return;
     } else {
         if (!cu(launch_any(d, a, d.stream), "filter kernel")) return;
@@ -325,6 +327,19 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         return fail(PF_ERR_ILLEGAL_CHARACTER);
     }
     if (bad_width) return;  // caller reports invalid parameters after all shards validated
+    if (dist) {
+        int32_t* dd = reinterpret_cast<int32_t*>(d.d_est);
+        if (!cu(sb::launch_edit_distance(d.d_text, d.d_pattern, pitch, a.n, a.m,
+                                         static_cast<int>(std::min<uint32_t>(e, 1u << 30)), dd,
+                                         d.stream),
+                "edit distance kernel"))
+            return;
+        if (!cu(cudaMemcpyAsync(dist + p0, dd, n * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                d.stream), "D2H distances"))
+            return;
+        cu(cudaStreamSynchronize(d.stream), "sync");
+        return;
+    }
     if (short_circuit) {
         if (!cu(sb::launch_accept_all(a.n, a.m, d.d_accept, estimates ? d.d_est : nullptr,
                                       bits ? d.d_bits : nullptr, d.stream),
@@ -454,20 +469,24 @@ void pf_ctx_destroy(pf_ctx* ctx) {
 
 int pf_ctx_device_count(const pf_ctx* ctx) { return ctx ? static_cast<int>(ctx->devs.size()) : 0; }
 
-int pf_shouji_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t stride,
-                           size_t n, uint32_t m, uint32_t e, uint32_t width,
-                           uint32_t* accept_bitmap, uint32_t* estimates, uint64_t* bits,
-                           pf_error* err) {
+}  // extern "C"
+
+namespace {
+
+int run_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t stride, size_t n,
+              uint32_t m, uint32_t e, uint32_t width, uint32_t* accept_bitmap, uint32_t* estimates,
+              uint64_t* bits, int32_t* dist, pf_error* err) {
     if (err) std::memset(err, 0, sizeof(*err));
     if (!ctx) return PF_ERR_NULL_ARGUMENT;
     if (n == 0) return PF_OK;
-    if (!text || !pattern || !accept_bitmap) return PF_ERR_NULL_ARGUMENT;
+    if (!text || !pattern || (!accept_bitmap && !dist)) return PF_ERR_NULL_ARGUMENT;
     if (m == 0) {  // packed_sequence::from_string("") (packed_sequence.cpp:8)
         set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
         return PF_ERR_EMPTY_SEQUENCE;
     }
-    if (stride < m || m >= (1u << 24)) {
-        set_err(err, PF_ERR_INVALID_PARAMETERS, "stride < m or m >= 2^24");
+    if (stride < m || m >= (1u << 24) || (dist && m > 1024)) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS,
+                dist ? "stride < m or m > 1024 (edit distance)" : "stride < m or m >= 2^24");
         return PF_ERR_INVALID_PARAMETERS;
     }
     std::lock_guard<std::mutex> lock(ctx->mu);
@@ -479,13 +498,13 @@ int pf_shouji_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* patt
     std::vector<ShardResult> res(nd);
     if (nd == 1) {
         run_host_shard(ctx->devs[0], text, pattern, stride, bounds[0], bounds[1], m, e, width,
-                       accept_bitmap, estimates, bits, &res[0]);
+                       accept_bitmap, estimates, bits, dist, &res[0]);
     } else {
         std::vector<std::thread> pool;
         for (size_t t = 0; t < nd; ++t)
             pool.emplace_back(run_host_shard, std::ref(ctx->devs[t]), text, pattern, stride,
                               bounds[t], bounds[t + 1], m, e, width, accept_bitmap, estimates, bits,
-                              &res[t]);
+                              dist, &res[t]);
         for (auto& th : pool) th.join();
     }
     // First failure in pair order wins (illegal characters are located per
@@ -497,11 +516,30 @@ int pf_shouji_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* patt
             return res[t].status;
         }
     }
-    if (width < 3 || width > 8) {  // window_zero_table ctor (shouji.cpp:9-15)
+    if (!dist && (width < 3 || width > 8)) {  // window_zero_table ctor (shouji.cpp:9-15)
         set_err(err, PF_ERR_INVALID_PARAMETERS, "window width must be in [3, 8]");
         return PF_ERR_INVALID_PARAMETERS;
     }
     return PF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pf_shouji_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t stride,
+                           size_t n, uint32_t m, uint32_t e, uint32_t width,
+                           uint32_t* accept_bitmap, uint32_t* estimates, uint64_t* bits,
+                           pf_error* err) {
+    return run_batch(ctx, text, pattern, stride, n, m, e, width, accept_bitmap, estimates, bits,
+                     nullptr, err);
+}
+
+int pf_banded_edit_distance_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern,
+                                  size_t stride, size_t n, uint32_t m, uint32_t e, int32_t* out,
+                                  pf_error* err) {
+    if (!out) return PF_ERR_NULL_ARGUMENT;
+    return run_batch(ctx, text, pattern, stride, n, m, e, 4, nullptr, nullptr, nullptr, out, err);
 }
 
 int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,

@@ -66,6 +66,9 @@ cudaError_t launch_bits_transpose(const uint32_t* outplanes, long long n, int m,
 // 16-byte-pitched layout the filter kernels read.
 cudaError_t launch_repitch(const uint8_t* src, size_t src_stride, uint8_t* dst, size_t dst_pitch,
                            long long n, int m, cudaStream_t s);
+// Exact Levenshtein distance per pair (Myers bit-vector); out[i] = d <= e ? d : -1.
+cudaError_t launch_edit_distance(const uint8_t* text, const uint8_t* pattern, size_t pitch,
+                                 long long n, int m, int e, int32_t* out, cudaStream_t s);
 // e >= m short-circuit outputs.
 cudaError_t launch_accept_all(long long n, int m, uint32_t* accept, uint32_t* estimates,
                               uint64_t* bits, cudaStream_t s);
