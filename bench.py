@@ -242,15 +242,33 @@ def run_reference_arm(args, rank, world):
 # ------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------
+def bench_device(local_rank: int) -> int:
+    """One GPU per rank; PF_BENCH_DEVICE pins every rank to one device (tests only)."""
+    return int(os.environ.get("PF_BENCH_DEVICE", local_rank))
+
+
+def reduce_max(values, dev, world):
+    """Max over ranks of a few floats (NCCL needs CUDA tensors, gloo CPU ones)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return list(values)
+    on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor(list(values), dtype=torch.float64, device=on)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import paper_1809_07858_b200 as pf
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    ctx = pf.Context([local_rank])
+    gpu = bench_device(local_rank)
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    ctx = pf.Context([gpu])
     n, m, e = args.pairs, args.m, args.e
     pitch = pf.device_pitch(m)
     # A dedicated stream: the kernels and the timing events must share it.
@@ -276,11 +294,11 @@ def run_ours(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize(dev)
 
-    gpu_index = local_rank
+    gpu_index = gpu
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     if vis:
         try:
-            gpu_index = int(vis.split(",")[local_rank])
+            gpu_index = int(vis.split(",")[gpu])
         except Exception:
             pass
     clocks = ClockSampler(gpu_index)
@@ -346,11 +364,7 @@ def run_ours(args, rank, world, local_rank):
             tw.append(time.perf_counter() - t0)
         t_e2e = (t_e2e0, time.perf_counter())
         assert (acc_h[: chk // 32] == a_ref).all()
-        e2e_s = sum(tw) / len(tw)
-        if world > 1:
-            tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
+        e2e_s = reduce_max([sum(tw) / len(tw)], dev, world)[0]
         e2e = {"value": world * n / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(2 * n * m), "d2h_bytes_per_step": int(4 * ((n + 31) // 32)),
                "ms_per_step": 1e3 * e2e_s,
@@ -361,10 +375,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- max over ranks ---------------------------------------------------------------
     step_ms = elapsed_ms / args.steps
     kern_avg_ms = float(np.mean(kern_ms))
-    if world > 1:
-        tt = torch.tensor([step_ms, kern_avg_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        step_ms, kern_avg_ms = float(tt[0]), float(tt[1])
+    step_ms, kern_avg_ms = reduce_max([step_ms, kern_avg_ms], dev, world)
     value = world * n / (step_ms * 1e-3)
 
     # ---- roofline -----------------------------------------------------------------------
@@ -451,8 +462,13 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        gpu = bench_device(local_rank)
+        torch.cuda.set_device(gpu)
+        backend = os.environ.get("PF_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:
