@@ -129,6 +129,26 @@ int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint
  * Writes lane-operations per second. */
 int pf_int_peak(pf_ctx* ctx, int op, double* ops_per_second);
 
+/* ---- Split stages (advanced callers) -------------------------------------
+ * The host batch call's upload stage, exposed on its own. pf_host_pack_nibbles
+ * packs ASCII records on the host's cores into nibble records (4 bits per
+ * base, pf_nibble_pitch(m) bytes per record: byte q of 32-bit word w holds the
+ * low nibbles of columns 8w+q and 8w+q+4), validating every byte like
+ * packed_sequence::from_string (proj/src/packed_sequence.cpp:19-29: first
+ * illegal byte in pair order, text before pattern). simd = 0 forces the
+ * portable path. pf_shouji_filter_nibbles_device filters nibble records
+ * already in device memory (stream-ordered, no validation: the host did it).
+ * pf_shouji_filter_batch packs large batches this way (PF_HOST_PACK=0 turns
+ * it off, =1 forces it). */
+size_t pf_nibble_pitch(uint32_t m);
+int pf_host_pack_nibbles(const uint8_t* text, const uint8_t* pattern, size_t stride, size_t n,
+                         uint32_t m, uint8_t* out_text, uint8_t* out_pattern, int simd,
+                         pf_error* err);
+int pf_shouji_filter_nibbles_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                                    size_t n, uint32_t m, uint32_t e, uint32_t width,
+                                    uint32_t* d_accept_bitmap, uint32_t* d_estimates, void* stream,
+                                    pf_error* err);
+
 /* Tight device row pitch for length-m records: round4(m). */
 size_t pf_device_pitch(uint32_t m);
 
@@ -193,6 +213,11 @@ void pf_dataset_free(pf_dataset* ds);
 /* Number of kernel launches issued by this process so far (all contexts);
  * bench.py reports the delta over its timed region. */
 uint64_t pf_launch_count(void);
+
+/* Bytes copied host->device and device->host by the host entry points
+ * (pf_shouji_filter_batch and friends) so far in this process; bench.py
+ * reports the per-step delta as the e2e transfer volume. Either may be NULL. */
+void pf_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@ from .api import (  # noqa: F401
     illegal_character_error,
     invalid_parameters_error,
     launch_count,
+    transfer_bytes,
     length_mismatch_error,
     max_window_width,
     min_window_width,
@@ -34,6 +35,9 @@ from .api import (  # noqa: F401
     shouji_filter_device,
     shouji_filter_device_async,
     int_peak,
+    nibble_pitch,
+    host_pack_nibbles,
+    shouji_filter_nibbles_device,
     threshold_too_large_error,
     unpack_bitmap,
     banded_edit_distance,

@@ -266,6 +266,13 @@ def launch_count() -> int:
     return int(L.lib.pf_launch_count())
 
 
+def transfer_bytes() -> tuple[int, int]:
+    """(host->device, device->host) bytes moved by the host entry points so far."""
+    h2d, d2h = C.c_uint64(), C.c_uint64()
+    L.lib.pf_transfer_bytes(C.byref(h2d), C.byref(d2h))
+    return int(h2d.value), int(d2h.value)
+
+
 def device_pitch(m: int) -> int:
     return int(L.lib.pf_device_pitch(m))
 
@@ -367,6 +374,44 @@ def shouji_filter_device_async(d_text: int, d_pattern: int, pitch: int, n: int, 
     ctx = ctx or default_context()
     _raise(L.lib.pf_shouji_filter_device_async(ctx.handle, d_text, d_pattern, pitch, n, m, int(e),
                                                int(width), d_accept, d_estimates, d_err_flag, stream))
+
+
+def nibble_pitch(m: int) -> int:
+    """Bytes per nibble record of length m (4 * ceil(m / 8))."""
+    return int(L.lib.pf_nibble_pitch(int(m)))
+
+
+def host_pack_nibbles(text, pattern, m: int | None = None, simd: bool = True):
+    """Upload stage on the host's cores: ASCII records -> nibble records
+    (u8[n, nibble_pitch(m)] each), validated like packed_sequence::from_string."""
+    text = _as_records(text)
+    pattern = _as_records(pattern)
+    if text.shape != pattern.shape:
+        raise length_mismatch_error("text and pattern record arrays differ in shape")
+    n, stride = text.shape
+    m = stride if m is None else int(m)
+    npitch = nibble_pitch(m)
+    ot = np.zeros((n, npitch), np.uint8)
+    op = np.zeros((n, npitch), np.uint8)
+    err = L.PfError()
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    st = L.lib.pf_host_pack_nibbles(ptr(text), ptr(pattern), stride, n, m, ptr(ot), ptr(op),
+                                    1 if simd else 0, C.byref(err))
+    _raise(st, err)
+    return ot, op
+
+
+def shouji_filter_nibbles_device(d_text: int, d_pattern: int, n: int, m: int, e: int,
+                                 d_accept: int, width: int = default_window_width,
+                                 d_estimates: int | None = None, stream: int | None = None,
+                                 ctx: Context | None = None) -> None:
+    """Filter nibble records already on the device (rows of nibble_pitch(m) bytes)."""
+    ctx = ctx or default_context()
+    err = L.PfError()
+    st = L.lib.pf_shouji_filter_nibbles_device(ctx.handle, d_text, d_pattern, n, m, int(e),
+                                               int(width), d_accept, d_estimates, stream,
+                                               C.byref(err))
+    _raise(st, err)
 
 
 def int_peak(op: str = "lop3", ctx: Context | None = None) -> float:

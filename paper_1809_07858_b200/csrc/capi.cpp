@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -18,7 +19,9 @@
 #include <vector>
 
 #include "../../include/shouji_b200.h"
+#include "host_pack.h"
 #include "kernels.cuh"
+#include "pack.cuh"
 
 namespace {
 
@@ -52,6 +55,12 @@ struct DeviceState {
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     sb::Pipeline pipe;           // pack/search overlap for large batches
     size_t pipe_words[2] = {0, 0};
+    // host-pack upload path: pinned nibble buffers, device nibble buffers, events
+    uint8_t* h_nib[2] = {nullptr, nullptr};
+    size_t h_nib_bytes = 0;
+    uint8_t* d_nib[2] = {nullptr, nullptr};
+    size_t d_nib_bytes[2] = {0, 0};
+    cudaEvent_t nib_ev[2] = {nullptr, nullptr};
 };
 
 }  // namespace
@@ -133,6 +142,15 @@ cudaError_t launch_any(DeviceState& d, sb::FilterArgs a, cudaStream_t s) {
     return sb::launch_filter(a, s);
 }
 
+// Bytes moved between host and device by the host entry points (bench.py
+// reports them per step; pf_transfer_bytes).
+std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
+
+cudaError_t xfer(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+    (kind == cudaMemcpyHostToDevice ? g_h2d : g_d2h).fetch_add(bytes, std::memory_order_relaxed);
+    return cudaMemcpyAsync(dst, src, bytes, kind, s);
+}
+
 bool is_pinned(const void* p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -140,6 +158,41 @@ bool is_pinned(const void* p) {
         return false;
     }
     return a.type == cudaMemoryTypeHost;
+}
+
+// Host packing upload path: PF_HOST_PACK=0 disables it, =1 forces it for any
+// batch size (A/B runs, tests); unset, batches of kHostPackMin pairs or more use it.
+int host_pack_mode() {
+    static const int v = [] {
+        const char* e = std::getenv("PF_HOST_PACK");
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    return v;
+}
+constexpr long long kHostPackMin = 1ll << 16;
+
+// Pairs per host-pack chunk (PF_HOST_CHUNK overrides; multiple of 256).
+long long host_chunk() {
+    static const long long v = [] {
+        const char* e = std::getenv("PF_HOST_CHUNK");
+        long long c = e ? std::atoll(e) : (1ll << 19);
+        c = std::max(256ll, c);
+        return (c + 255) / 256 * 256;
+    }();
+    return v;
+}
+
+void set_illegal(pf_error* err, uint64_t pair, uint32_t field, uint64_t pos, uint8_t byte) {
+    if (!err) return;
+    err->status = PF_ERR_ILLEGAL_CHARACTER;
+    err->pair = pair;
+    err->field = field;
+    err->position = pos;
+    err->byte = byte;
+    std::snprintf(err->message, sizeof(err->message),
+                  "illegal character '%c' at position %llu of %s %llu",
+                  (byte >= 32 && byte < 127) ? byte : '?', (unsigned long long)pos,
+                  field == 0 ? "text" : "pattern", (unsigned long long)pair);
 }
 
 // Decode the locator key and fill err (the byte is read from the records).
@@ -155,17 +208,7 @@ void decode_illegal(unsigned long long key, long long pair_base, const uint8_t* 
         byte = *src;
     else
         cudaMemcpy(&byte, src, 1, cudaMemcpyDeviceToHost);
-    if (err) {
-        err->status = PF_ERR_ILLEGAL_CHARACTER;
-        err->pair = pair + static_cast<uint64_t>(pair_base);
-        err->field = field;
-        err->position = pos;
-        err->byte = byte;
-        std::snprintf(err->message, sizeof(err->message),
-                      "illegal character '%c' at position %llu of %s %llu",
-                      (byte >= 32 && byte < 127) ? byte : '?', (unsigned long long)pos,
-                      field == 0 ? "text" : "pattern", (unsigned long long)err->pair);
-    }
+    set_illegal(err, pair + static_cast<uint64_t>(pair_base), field, pos, byte);
 }
 
 struct ShardResult {
@@ -195,8 +238,14 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         fail(ce == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA);
         return false;
     };
-    if (!cu(grow(d.d_text, d.in_bytes, n * pitch), "alloc text")) return;
-    if (!cu(grow(d.d_pattern, d.in_pattern_bytes, n * pitch), "alloc pattern")) return;
+    const int hp_mode = host_pack_mode();
+    const bool host_pack = hp_mode != 0 && !dist && e < m && width >= 3 && width <= 8 && !bits &&
+                           sb::nibble_pack_fits(static_cast<int>(m)) &&
+                           (hp_mode == 1 || static_cast<long long>(n) >= kHostPackMin);
+    if (!host_pack) {
+        if (!cu(grow(d.d_text, d.in_bytes, n * pitch), "alloc text")) return;
+        if (!cu(grow(d.d_pattern, d.in_pattern_bytes, n * pitch), "alloc pattern")) return;
+    }
     const size_t ngroups = (n + 31) / 32;
     if (!cu(grow(d.d_accept, d.accept_words, ngroups), "alloc accept")) return;
     if ((estimates || dist) && !cu(grow(d.d_est, d.est_n, n), "alloc estimates")) return;
@@ -211,6 +260,90 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         if (!cu(cudaMalloc(&d.d_key, sizeof(unsigned long long)), "alloc key")) return;
     }
 
+    // ---- host packing upload path ---------------------------------------------
+    // The host's cores pack records into nibble records (host_pack.cpp, half
+    // the bytes) chunk by chunk into pinned buffers; chunk i's DMA, device pack
+    // and search run on the stream while the cores pack chunk i+1.
+    if (host_pack) {
+        // pairs per chunk; a multiple of 256 so the pattern rows (at chunk * np)
+        // stay 16-byte aligned for the pack kernel's bulk copies
+        const long long chunk =
+            std::min<long long>((static_cast<long long>(n) + 255) / 256 * 256, host_chunk());
+        const size_t np = sb::nibble_pitch(static_cast<int>(m));
+        const size_t cbytes = 2 * static_cast<size_t>(chunk) * np;  // text rows, then pattern rows
+        if (d.h_nib_bytes < cbytes) {
+            for (int b = 0; b < 2; ++b) {
+                if (d.h_nib[b]) cudaFreeHost(d.h_nib[b]);
+                d.h_nib[b] = nullptr;
+            }
+            d.h_nib_bytes = 0;
+            for (int b = 0; b < 2; ++b)
+                if (!cu(cudaHostAlloc(&d.h_nib[b], cbytes, cudaHostAllocPortable), "alloc host nibbles"))
+                    return;
+            d.h_nib_bytes = cbytes;
+        }
+        for (int b = 0; b < 2; ++b) {
+            if (!cu(grow(d.d_nib[b], d.d_nib_bytes[b], cbytes), "alloc device nibbles")) return;
+            if (!d.nib_ev[b] &&
+                !cu(cudaEventCreateWithFlags(&d.nib_ev[b], cudaEventDisableTiming), "event"))
+                return;
+        }
+        if (!cu(grow(d.d_scratch, d.scratch_words, sb::planes_scratch_words(chunk, m)),
+                "alloc planes"))
+            return;
+        const uint8_t* tsrc0 = text + p0 * stride;
+        const uint8_t* psrc0 = pattern + p0 * stride;
+        const long long nchunks = (static_cast<long long>(n) + chunk - 1) / chunk;
+        for (long long i = 0; i < nchunks; ++i) {
+            const int b = static_cast<int>(i & 1);
+            const long long lo = i * chunk;
+            const long long cn = std::min<long long>(chunk, static_cast<long long>(n) - lo);
+            // the DMA that last read this pinned buffer (chunk i-2) must be done
+            if (i >= 2 && !cu(cudaEventSynchronize(d.nib_ev[b]), "nibble buffer wait")) return;
+            uint8_t* ht = d.h_nib[b];
+            uint8_t* hq = ht + static_cast<size_t>(chunk) * np;
+            sb::HostBad bad;
+            sb::host_pack_nibbles_parallel(tsrc0 + lo * stride, psrc0 + lo * stride, stride, cn,
+                                           static_cast<int>(m), ht, hq, &bad);
+            if (bad.any) {  // chunks run in pair order: the first chunk with a bad byte wins
+                cu(cudaStreamSynchronize(d.stream), "sync");
+                set_illegal(err, p0 + lo + bad.pair, static_cast<uint32_t>(bad.field),
+                            static_cast<uint64_t>(bad.pos), bad.byte);
+                return fail(PF_ERR_ILLEGAL_CHARACTER);
+            }
+            const size_t cb = static_cast<size_t>(cn) * np;
+            if (!cu(xfer(d.d_nib[b], ht, cb, cudaMemcpyHostToDevice, d.stream), "H2D nibbles"))
+                return;
+            if (!cu(xfer(d.d_nib[b] + static_cast<size_t>(chunk) * np, hq, cb,
+                         cudaMemcpyHostToDevice, d.stream), "H2D nibbles"))
+                return;
+            if (!cu(cudaEventRecord(d.nib_ev[b], d.stream), "nibble record")) return;
+            sb::FilterArgs a{};
+            a.text = d.d_nib[b];
+            a.pattern = d.d_nib[b] + static_cast<size_t>(chunk) * np;
+            a.pitch = np;
+            a.nibbles = true;
+            a.n = cn;
+            a.m = static_cast<int>(m);
+            a.e = e;
+            a.width = width;
+            a.accept = d.d_accept + lo / 32;
+            a.estimates = estimates ? d.d_est + lo : nullptr;
+            a.planes = d.d_scratch;
+            a.planes_words = d.scratch_words;
+            if (!cu(sb::launch_filter(a, d.stream), "filter kernel")) return;
+        }
+        if (!cu(xfer(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, d.stream), "D2H accept"))
+            return;
+        if (estimates &&
+            !cu(xfer(estimates + p0, d.d_est, n * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, d.stream), "D2H estimates"))
+            return;
+        cu(cudaStreamSynchronize(d.stream), "sync");
+        return;
+    }
+
     // ---- host -> device ----------------------------------------------------
     // Records land in the device layout (pitch = round16(m)). A caller buffer
     // already in that layout is one DMA per sequence; otherwise rows are
@@ -222,9 +355,9 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     const uint8_t* psrc = pattern + p0 * stride;
     if (pinned && stride == pitch) {
         const size_t bytes = (n - 1) * pitch + m;
-        if (!cu(cudaMemcpyAsync(d.d_text, tsrc, bytes, cudaMemcpyHostToDevice, d.stream), "H2D text"))
+        if (!cu(xfer(d.d_text, tsrc, bytes, cudaMemcpyHostToDevice, d.stream), "H2D text"))
             return;
-        if (!cu(cudaMemcpyAsync(d.d_pattern, psrc, bytes, cudaMemcpyHostToDevice, d.stream),
+        if (!cu(xfer(d.d_pattern, psrc, bytes, cudaMemcpyHostToDevice, d.stream),
                 "H2D pattern"))
             return;
     } else {
@@ -268,9 +401,9 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             const size_t bytes = (nr - 1) * sstride + m;
             uint8_t* dt = d.d_stage;
             uint8_t* dp = d.d_stage + rows * sstride;
-            if (!cu(cudaMemcpyAsync(dt, st, bytes, cudaMemcpyHostToDevice, d.stream), "H2D text"))
+            if (!cu(xfer(dt, st, bytes, cudaMemcpyHostToDevice, d.stream), "H2D text"))
                 return;
-            if (!cu(cudaMemcpyAsync(dp, sp, bytes, cudaMemcpyHostToDevice, d.stream), "H2D pattern"))
+            if (!cu(xfer(dp, sp, bytes, cudaMemcpyHostToDevice, d.stream), "H2D pattern"))
                 return;
             if (!pinned && !cu(cudaEventRecord(d.stage_ev[buf], d.stream), "stage record")) return;
             if (!cu(sb::launch_repitch(dt, sstride, d.d_text + r0 * pitch, pitch,
@@ -308,7 +441,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         if (!cu(launch_any(d, a, d.stream), "filter kernel")) return;
     }
     uint32_t flag = 0;
-    if (!cu(cudaMemcpyAsync(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, d.stream),
+    if (!cu(xfer(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, d.stream),
             "D2H flag"))
         return;
     if (!cu(cudaStreamSynchronize(d.stream), "sync")) return;
@@ -319,7 +452,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
                 "locate"))
             return;
         unsigned long long key = 0;
-        if (!cu(cudaMemcpyAsync(&key, d.d_key, sizeof(key), cudaMemcpyDeviceToHost, d.stream),
+        if (!cu(xfer(&key, d.d_key, sizeof(key), cudaMemcpyDeviceToHost, d.stream),
                 "D2H key"))
             return;
         if (!cu(cudaStreamSynchronize(d.stream), "sync")) return;
@@ -334,7 +467,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
                                          d.stream),
                 "edit distance kernel"))
             return;
-        if (!cu(cudaMemcpyAsync(dist + p0, dd, n * sizeof(int32_t), cudaMemcpyDeviceToHost,
+        if (!cu(xfer(dist + p0, dd, n * sizeof(int32_t), cudaMemcpyDeviceToHost,
                                 d.stream), "D2H distances"))
             return;
         cu(cudaStreamSynchronize(d.stream), "sync");
@@ -351,15 +484,15 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     }
 
     // ---- device -> host ------------------------------------------------------
-    if (!cu(cudaMemcpyAsync(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
+    if (!cu(xfer(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
                             cudaMemcpyDeviceToHost, d.stream), "D2H accept"))
         return;
     if (estimates &&
-        !cu(cudaMemcpyAsync(estimates + p0, d.d_est, n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+        !cu(xfer(estimates + p0, d.d_est, n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                             d.stream), "D2H estimates"))
         return;
     if (bits &&
-        !cu(cudaMemcpyAsync(bits + p0 * wpp, d.d_bits, n * wpp * sizeof(uint64_t),
+        !cu(xfer(bits + p0 * wpp, d.d_bits, n * wpp * sizeof(uint64_t),
                             cudaMemcpyDeviceToHost, d.stream), "D2H bits"))
         return;
     cu(cudaStreamSynchronize(d.stream), "sync");
@@ -398,6 +531,75 @@ int pf_device_count(void) {
 size_t pf_device_pitch(uint32_t m) { return round_up(std::max<uint32_t>(m, 1), 4); }
 
 uint64_t pf_launch_count(void) { return sb::launch_count(); }
+
+void pf_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
+    if (h2d) *h2d = g_h2d.load();
+    if (d2h) *d2h = g_d2h.load();
+}
+
+size_t pf_nibble_pitch(uint32_t m) { return sb::nibble_pitch(static_cast<int>(std::max<uint32_t>(m, 1))); }
+
+int pf_host_pack_nibbles(const uint8_t* text, const uint8_t* pattern, size_t stride, size_t n,
+                         uint32_t m, uint8_t* out_text, uint8_t* out_pattern, int simd,
+                         pf_error* err) {
+    if (err) std::memset(err, 0, sizeof(*err));
+    if (n == 0) return PF_OK;
+    if (!text || !pattern || !out_text || !out_pattern) return PF_ERR_NULL_ARGUMENT;
+    if (m == 0) {
+        set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
+        return PF_ERR_EMPTY_SEQUENCE;
+    }
+    if (stride < m) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS, "stride < m");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    sb::HostBad bad;
+    sb::host_pack_nibbles_parallel(text, pattern, stride, static_cast<long long>(n),
+                                   static_cast<int>(m), out_text, out_pattern, &bad, 0, simd != 0);
+    if (bad.any) {
+        set_illegal(err, bad.pair, static_cast<uint32_t>(bad.field), static_cast<uint64_t>(bad.pos),
+                    bad.byte);
+        return PF_ERR_ILLEGAL_CHARACTER;
+    }
+    return PF_OK;
+}
+
+int pf_shouji_filter_nibbles_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                                    size_t n, uint32_t m, uint32_t e, uint32_t width,
+                                    uint32_t* d_accept_bitmap, uint32_t* d_estimates, void* stream,
+                                    pf_error* err) {
+    if (err) std::memset(err, 0, sizeof(*err));
+    if (!ctx) return PF_ERR_NULL_ARGUMENT;
+    if (n == 0) return PF_OK;
+    if (!d_text || !d_pattern || !d_accept_bitmap) return PF_ERR_NULL_ARGUMENT;
+    if (m == 0 || e >= m || width < 3 || width > 8 || !sb::nibble_pack_fits(static_cast<int>(m)) ||
+        reinterpret_cast<uintptr_t>(d_text) % 16 || reinterpret_cast<uintptr_t>(d_pattern) % 16) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS,
+                "nibble path needs e < m, 3 <= width <= 8, a record that fits a pack tile and "
+                "16-byte aligned record arrays");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceState& d = ctx->devs[0];
+    PF_CUDA(cudaSetDevice(d.device));
+    PF_CUDA(grow(d.d_scratch, d.scratch_words,
+                 sb::planes_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
+    sb::FilterArgs a{};
+    a.text = d_text;
+    a.pattern = d_pattern;
+    a.pitch = sb::nibble_pitch(static_cast<int>(m));
+    a.nibbles = true;
+    a.n = static_cast<long long>(n);
+    a.m = static_cast<int>(m);
+    a.e = e;
+    a.width = width;
+    a.accept = d_accept_bitmap;
+    a.estimates = d_estimates;
+    a.planes = d.d_scratch;
+    a.planes_words = d.scratch_words;
+    PF_CUDA(sb::launch_filter(a, static_cast<cudaStream_t>(stream)));
+    return PF_OK;
+}
 
 int pf_ctx_create(const int* devices, int count, pf_ctx** out) {
     if (!out) return PF_ERR_NULL_ARGUMENT;
@@ -451,6 +653,11 @@ void pf_ctx_destroy(pf_ctx* ctx) {
         cudaFree(d.d_flag);
         cudaFree(d.d_key);
         cudaFree(d.d_stage);
+        for (int b = 0; b < 2; ++b) {
+            if (d.h_nib[b]) cudaFreeHost(d.h_nib[b]);
+            cudaFree(d.d_nib[b]);
+            if (d.nib_ev[b]) cudaEventDestroy(d.nib_ev[b]);
+        }
         cudaFree(d.pipe.planes[0]);
         cudaFree(d.pipe.planes[1]);
         cudaEvent_t evs[] = {d.pipe.start, d.pipe.done, d.pipe.packed[0], d.pipe.packed[1],

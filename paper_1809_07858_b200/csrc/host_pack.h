@@ -1,0 +1,44 @@
+// Host packing stage: ASCII records -> nibble records on the CPU (see host_pack.cpp).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace sb {
+
+// First illegal byte seen, in the reference's order: lowest pair, text (field
+// 0) before pattern (field 1), lowest position.
+struct HostBad {
+    bool any = false;
+    uint64_t pair = 0;
+    int field = 0;
+    int pos = 0;
+    uint8_t byte = 0;
+    void offer(uint64_t p, int f, int q, uint8_t b) {
+        if (!any || p < pair || (p == pair && (f < field || (f == field && q < pos)))) {
+            any = true;
+            pair = p;
+            field = f;
+            pos = q;
+            byte = b;
+        }
+    }
+};
+
+// Pack pairs [lo, hi) of a batch into nibble records (pack.cuh nibble format,
+// row pitch nibble_pitch(m)); out_text/out_pattern point at the batch's row 0.
+// Thread-safe for disjoint pair ranges.
+void host_pack_nibbles(const uint8_t* text, const uint8_t* pattern, size_t stride, int m,
+                       long long lo, long long hi, uint8_t* out_text, uint8_t* out_pattern,
+                       HostBad* bad, bool allow_simd = true);
+
+// All n pairs on the process-wide worker pool (threads = 0: all hardware
+// threads). bad receives the first illegal byte in pair order.
+void host_pack_nibbles_parallel(const uint8_t* text, const uint8_t* pattern, size_t stride,
+                                long long n, int m, uint8_t* out_text, uint8_t* out_pattern,
+                                HostBad* bad, unsigned threads = 0, bool allow_simd = true);
+unsigned host_pack_threads();
+
+// True when the AVX-512 (BW/VBMI) path is used on this host.
+bool host_pack_uses_simd();
+
+}  // namespace sb

@@ -26,6 +26,7 @@ struct FilterArgs {
     uint32_t* err_flag;    // device, 1 word, zeroed by the caller
     uint32_t* planes;      // device scratch for the pair-sliced planes (pack.cuh)
     size_t planes_words;   // available words in planes
+    bool nibbles;          // text/pattern are host-packed nibble records (pitch unused)
 };
 
 // Scratch words the filter needs for n pairs of length m.
@@ -35,6 +36,10 @@ bool use_fused(uint32_t width, uint32_t e, int m);
 // Stage 1: records -> planes (planes may be null: validation only).
 cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
                         int m, uint32_t* planes, uint32_t* err_flag, cudaStream_t s);
+// Stage 1 from nibble records (pack.cuh nibble format; no validation).
+bool nibble_pack_fits(int m);
+cudaError_t launch_pack_nibbles(const uint8_t* text, const uint8_t* pattern, long long n, int m,
+                                uint32_t* planes, cudaStream_t s);
 // Launch the filter (pack + width-4 search, or pack + generic). Returns a cudaError_t.
 cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s);
 // Resources for the chunked, two-stream pipeline: pack of chunk i+1 (memory

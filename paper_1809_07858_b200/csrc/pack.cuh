@@ -18,9 +18,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
-
-#include "phase_a.cuh"
 
 namespace sb {
 
@@ -28,8 +27,9 @@ constexpr int kPackPairs = 256;                 // pairs per pair block (CTA)
 constexpr int kPackGroups = kPackPairs / 32;    // groups per pair block
 constexpr int kPackNT = 128;                    // threads per pack CTA
 
-// Columns stored per pair (chunk-rounded).
-__host__ __device__ inline int plane_cols(int m) { return (m + CH - 1) / CH * CH; }
+// Column stride of the planes layout: exactly m (only columns < m are ever
+// written or read).
+__host__ __device__ inline int plane_cols(int m) { return m; }
 
 // Words of plane storage for n pairs of length m (both sequences).
 inline size_t plane_words(long long n, int m) {
@@ -44,5 +44,13 @@ __host__ __device__ inline size_t plane_index(int s, long long g, int col, int k
     return ((static_cast<size_t>(s) * nblocks + blk) * mc + col) * (3 * kPackGroups) +
            k * kPackGroups + (g % kPackGroups);
 }
+
+// Nibble records: the upload format of host-packed batches (host_pack.cpp).
+// A record of m columns is ceil(m/8) little-endian uint32 words; byte q of
+// word w holds the low nibbles of columns 8w+q (bits 0-3) and 8w+q+4 (bits
+// 4-7); columns >= m are zero. Bits 1-3 of a nibble are bits 1-3 of the ASCII
+// byte (lo, hi, N), so the device gather needs only a different shift per
+// column. Validation happens on the host, which packs.
+__host__ __device__ inline size_t nibble_pitch(int m) { return 4 * static_cast<size_t>((m + 7) / 8); }
 
 }  // namespace sb

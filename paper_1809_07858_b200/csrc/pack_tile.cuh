@@ -59,9 +59,18 @@ __host__ __device__ inline size_t seq_stride(size_t pitch, int groups) {
 inline size_t tile_smem(size_t pitch, int groups) { return 2 * seq_stride(pitch, groups) + 128; }
 inline int tile_groups(size_t pitch) { return pitch <= 128 ? 8 : 4; }
 
-template <bool EDGE, int ALIGN>
+template <bool EDGE, int ALIGN, bool NIB = false>
 __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size_t pitch, int col0,
                                                int m, uint32_t* dst, int stride) {
+    if constexpr (NIB) {
+        switch (ncg) {
+            case 1: gather_chunk_nib<EDGE, 1>(src, pitch, col0, m, dst, stride); break;
+            case 2: gather_chunk_nib<EDGE, 2>(src, pitch, col0, m, dst, stride); break;
+            case 3: gather_chunk_nib<EDGE, 3>(src, pitch, col0, m, dst, stride); break;
+            default: gather_chunk_nib<EDGE, 4>(src, pitch, col0, m, dst, stride); break;
+        }
+        return 0u;
+    }
     switch (ncg) {
         case 1: return gather_chunk<EDGE, false, 1, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
         case 2: return gather_chunk<EDGE, false, 2, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
@@ -73,8 +82,9 @@ __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size
 // Pack one tile of GROUPS x 32 pairs starting at group g0 (all threads of the
 // CTA call it; NT threads). sm: tile_smem() bytes of dynamic shared memory;
 // bar: an initialised mbarrier; parity: its current phase (flipped on return
-// by the caller). Returns nonzero on an illegal byte.
-template <int ALIGN, int NT>
+// by the caller). Returns nonzero on an illegal byte. NIB: the records are
+// nibble records (pack.cuh; pitch = nibble_pitch(m)), validated by the host.
+template <int ALIGN, int NT, bool NIB = false>
 __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, uint32_t parity,
                                                   int GROUPS, long long g0,
                                                   const uint8_t* __restrict__ text,
@@ -130,7 +140,7 @@ __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, ui
     // Items are (chunk, group, sequence) tiles of 32 pairs x 16 columns, the
     // sequence fastest. Full chunks come first and the one chunk straddling m
     // (if any) last, so no warp mixes the gather variants.
-    const int C = mc / CH;
+    const int C = (mc + CH - 1) / CH;
     const int Cfull = m / CH;  // chunks entirely inside [0, m)
     uint32_t err = 0u;
     uint32_t sink[CH * 3];
@@ -140,12 +150,16 @@ __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, ui
         const int sq = it % 2;
         uint32_t* dst = planes ? planes + plane_index(sq, g0 + g, c * CH, 0, nblocks, mc) : sink;
         const int stride = planes ? kPackGroups : 1;
-        if (c < Cfull)
-            err |= gather_chunk<false, false, 4, ALIGN>(rec(sq, g), pitch, 0, 32, c * CH, m, dst,
-                                                         stride);
-        else
-            err |= gather_ncg<true, ALIGN>((m - c * CH + 3) / 4, rec(sq, g), pitch, c * CH, m, dst,
-                                           stride);
+        if (c < Cfull) {
+            if constexpr (NIB)
+                gather_chunk_nib<false, 4>(rec(sq, g), pitch, c * CH, m, dst, stride);
+            else
+                err |= gather_chunk<false, false, 4, ALIGN>(rec(sq, g), pitch, 0, 32, c * CH, m,
+                                                             dst, stride);
+        } else {
+            err |= gather_ncg<true, ALIGN, NIB>((m - c * CH + 3) / 4, rec(sq, g), pitch, c * CH, m,
+                                                dst, stride);
+        }
     }
     return err;
 }

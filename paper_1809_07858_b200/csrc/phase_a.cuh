@@ -147,6 +147,69 @@ __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq
     return err;
 }
 
+// gather_chunk for nibble records (pack.cuh nibble format, validated on the
+// host): a 16-column chunk is two words per row; column group cg (4 columns)
+// is word cg/2, low nibbles for even cg, high nibbles for odd cg, so ASCII bit
+// k of column 4cg+q sits at bit 8q + 4(cg&1) + k of the word and reaches bit
+// 8q+i of the plane-k accumulator by one shift, as in gather_chunk.
+template <bool EDGE, int NCG>
+__device__ __forceinline__ void gather_chunk_nib(const uint8_t* __restrict__ seq, size_t pitch,
+                                                 int col0, int m, uint32_t* __restrict__ dst,
+                                                 int dstride) {
+    constexpr int NW = (NCG + 1) / 2;
+    uint32_t O[NCG][3][4];
+#pragma unroll
+    for (int cg = 0; cg < NCG; ++cg)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) O[cg][k][q] = 0u;
+#pragma unroll 1
+    for (int g8 = 0; g8 < 4; ++g8) {
+        uint32_t v[8][NW];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t* q =
+                reinterpret_cast<const uint32_t*>(seq + (8 * g8 + i) * pitch + col0 / 2);
+#pragma unroll
+            for (int w = 0; w < NW; ++w) v[i][w] = q[w];
+        }
+        uint32_t acc[3][NCG];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int cg = 0; cg < NCG; ++cg) acc[k][cg] = 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int cg = 0; cg < NCG; ++cg) {
+                const uint32_t w = v[i][cg / 2];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const int s = i - (k + 1) - 4 * (cg & 1);
+                    const uint32_t u = s >= 0 ? w * (1u << s) : __umulhi(w, 1u << (32 + s));
+                    acc[k][cg] |= u & (0x01010101u << i);
+                }
+            }
+#pragma unroll
+        for (int cg = 0; cg < NCG; ++cg)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    O[cg][k][q] = __byte_perm(O[cg][k][q], acc[k][cg], 0x0321 | ((4 + q) << 12));
+    }
+#pragma unroll
+    for (int cg = 0; cg < NCG; ++cg)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int col = 4 * cg + q;
+            if (EDGE && col0 + col >= m) continue;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) dst[(col * 3 + k) * dstride] = O[cg][k][q];
+        }
+}
+
 // A chunk entirely outside [0, m): every column is N.
 __device__ __forceinline__ void fill_oob_chunk(uint32_t* __restrict__ dst, int dstride) {
 #pragma unroll

@@ -1,0 +1,124 @@
+"""GPU parity of the host-pack upload path: records packed into nibble records
+on the host's cores (csrc/host_pack.cpp), filtered on the device from nibbles
+(pack.cuh nibble format, phase_a.cuh gather_chunk_nib) — against the oracle.
+
+pf_shouji_filter_batch routes host batches of >= 65536 pairs through this path
+(PF_HOST_PACK unset), so the large-batch tests below exercise it end to end,
+including chunk boundaries (512Ki pairs per chunk) and error order across chunks.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ACGT = np.frombuffer(b"ACGT", np.uint8)
+ACGTN = np.frombuffer(b"ACGTN", np.uint8)
+
+
+def mutated(rng, n, m, rate=0.06, alphabet=ACGTN):
+    t = alphabet[rng.integers(0, len(alphabet), size=(n, m))]
+    p = t.copy()
+    mask = rng.random(p.shape) < rate
+    p[mask] = ACGT[rng.integers(0, 4, size=int(mask.sum()))]
+    # some shifted patterns (indels) so the diagonals matter
+    for i in range(0, n, 7):
+        s = int(rng.integers(-3, 4))
+        p[i] = np.roll(p[i], s)
+    return np.ascontiguousarray(t), np.ascontiguousarray(p)
+
+
+def run_nibbles(gpu, t, p, e, width=4):
+    import torch
+    n, m = t.shape
+    nt, npat = gpu.host_pack_nibbles(t, p)
+    dt = torch.from_numpy(nt).cuda()
+    dp = torch.from_numpy(npat).cuda()
+    acc = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    est = torch.zeros(n, dtype=torch.int32, device="cuda")
+    gpu.shouji_filter_nibbles_device(dt.data_ptr(), dp.data_ptr(), n, m, e, acc.data_ptr(),
+                                     width=width, d_estimates=est.data_ptr())
+    torch.cuda.synchronize()
+    return acc.cpu().numpy().view(np.uint32), est.cpu().numpy().view(np.uint32)
+
+
+@pytest.mark.parametrize("m", [1, 2, 5, 8, 9, 15, 16, 17, 31, 33, 64, 100, 127, 128, 129, 150,
+                               250, 255, 256, 300, 512])
+def test_nibble_device_path_lengths(gpu, oracle, m):
+    rng = np.random.default_rng(m)
+    n = 2000 + 3 * m + 5  # ragged last tile
+    t, p = mutated(rng, n, m)
+    for e in sorted({0, min(m - 1, 1), min(m - 1, 3), min(m - 1, 9), m - 1}):
+        a1, e1 = run_nibbles(gpu, t, p, e)
+        a2, e2, _ = oracle.shouji_batch(t, p, e)
+        assert (a1 == a2).all(), (m, e)
+        assert (e1 == e2).all(), (m, e)
+
+
+@pytest.mark.parametrize("width", [3, 5, 6, 7, 8])
+def test_nibble_device_path_widths(gpu, oracle, width):
+    rng = np.random.default_rng(100 + width)
+    t, p = mutated(rng, 3001, 100)
+    for e in (2, 5, 12):
+        a1, e1 = run_nibbles(gpu, t, p, e, width)
+        a2, e2, _ = oracle.shouji_batch(t, p, e, width)
+        assert (a1 == a2).all() and (e1 == e2).all(), (width, e)
+
+
+def test_nibble_device_path_rejects_bad_parameters(gpu):
+    import torch
+    buf = torch.zeros(1024, dtype=torch.uint8, device="cuda")
+    acc = torch.zeros(4, dtype=torch.int32, device="cuda")
+    for m, e, w in [(10, 10, 4), (10, 3, 2), (10, 3, 9), (0, 0, 4)]:
+        with pytest.raises(gpu.invalid_parameters_error):
+            gpu.shouji_filter_nibbles_device(buf.data_ptr(), buf.data_ptr(), 32, m, e,
+                                             acc.data_ptr(), width=w)
+    with pytest.raises(gpu.invalid_parameters_error):  # bulk copies need 16-byte aligned bases
+        gpu.shouji_filter_nibbles_device(buf.data_ptr() + 4, buf.data_ptr(), 32, 10, 3,
+                                         acc.data_ptr())
+
+
+@pytest.mark.parametrize("n", [65536, 65536 + 31, 1_200_001])
+def test_host_batch_uses_nibbles_and_matches(gpu, oracle, n):
+    rng = np.random.default_rng(n)
+    t, p = mutated(rng, n, 100, alphabet=ACGT)
+    before = gpu.launch_count()
+    h0, _ = gpu.transfer_bytes()
+    a1, e1, _ = gpu.shouji_filter_batch(t, p, 5, estimates=True)
+    assert gpu.launch_count() > before
+    h1, _ = gpu.transfer_bytes()
+    assert h1 - h0 == 2 * n * gpu.nibble_pitch(100)  # nibble records crossed PCIe, not ASCII
+    a2, e2, _ = oracle.shouji_batch(t, p, 5)
+    assert (a1 == a2).all() and (e1 == e2).all()
+
+
+def test_host_batch_pinned_and_strided(gpu, oracle):
+    import torch
+    rng = np.random.default_rng(5)
+    n, m, stride = 300_000, 150, 157
+    t, p = mutated(rng, n, m)
+    bt = torch.full((n, stride), ord("q"), dtype=torch.uint8).pin_memory()
+    bp = torch.full((n, stride), ord("q"), dtype=torch.uint8).pin_memory()
+    bt.numpy()[:, :m] = t
+    bp.numpy()[:, :m] = p
+    a1, e1, _ = gpu.shouji_filter_batch(bt.numpy(), bp.numpy(), 7, m=m, estimates=True)
+    a2, e2, _ = oracle.shouji_batch(t, p, 7)
+    assert (a1 == a2).all() and (e1 == e2).all()
+
+
+def test_host_batch_first_illegal_byte_across_chunks(gpu):
+    rng = np.random.default_rng(11)
+    n, m = 1_100_000, 100
+    t = np.ascontiguousarray(ACGT[rng.integers(0, 4, size=(n, m))])
+    p = t.copy()
+    p[1_050_000, 5] = ord("x")   # third chunk
+    t[700_000, 99] = ord("-")    # second chunk: reported first
+    with pytest.raises(gpu.illegal_character_error) as ei:
+        gpu.shouji_filter_batch(t, p, 5)
+    err = ei.value
+    assert (err.pair, err.field, err.position(), err.byte()) == (700_000, 0, 99, "-")
+    t[700_000, 99] = ord("A")
+    with pytest.raises(gpu.illegal_character_error) as ei:
+        gpu.shouji_filter_batch(t, p, 5)
+    assert (ei.value.pair, ei.value.field, ei.value.position()) == (1_050_000, 1, 5)
+    p[1_050_000, 5] = ord("A")
+    gpu.shouji_filter_batch(t, p, 5)  # and the context still works
