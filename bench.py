@@ -467,6 +467,10 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if local_world > 1 and "PF_HOST_THREADS" not in os.environ:
+        # ranks on one host share its cores for the host-pack upload stage
+        os.environ["PF_HOST_THREADS"] = str(max(1, (os.cpu_count() or 1) // local_world))
     if world > 1:
         import torch
         import torch.distributed as dist

@@ -175,7 +175,7 @@ constexpr long long kHostPackMin = 1ll << 16;
 long long host_chunk() {
     static const long long v = [] {
         const char* e = std::getenv("PF_HOST_CHUNK");
-        long long c = e ? std::atoll(e) : (1ll << 19);
+        long long c = e ? std::atoll(e) : (1ll << 18);
         c = std::max(256ll, c);
         return (c + 255) / 256 * 256;
     }();

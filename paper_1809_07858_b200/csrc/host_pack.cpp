@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <functional>
@@ -211,8 +212,15 @@ private:
     bool stop_ = false;
 };
 
+// Threads = hardware threads, or PF_HOST_THREADS (e.g. cores / ranks when
+// several processes share the host).
 Pool& pool() {
-    static Pool p(std::max(1u, std::thread::hardware_concurrency()) - 1);
+    static Pool p([] {
+        const char* e = std::getenv("PF_HOST_THREADS");
+        const long v = e ? std::atol(e) : 0;
+        const unsigned n = v > 0 ? static_cast<unsigned>(v) : std::thread::hardware_concurrency();
+        return std::max(1u, n) - 1;
+    }());
     return p;
 }
 

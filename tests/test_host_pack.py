@@ -138,3 +138,26 @@ def test_host_pack_errors():
     assert L.lib.pf_host_pack_nibbles(None, vp, 10, 4, 10, op, op, 1, C.byref(err)) == \
         L.PF_ERR_NULL_ARGUMENT
     assert L.lib.pf_host_pack_nibbles(vp, vp, 10, 0, 10, op, op, 1, C.byref(err)) == L.PF_OK
+
+
+@pytest.mark.parametrize("offset", [0, 4, 8, 52, 60])
+def test_host_pack_output_alignment(offset):
+    """Any destination alignment gives the same bytes and nothing is written
+    outside the rows (the 64-byte masked stores stop at each row's end)."""
+    rng = np.random.default_rng(offset)
+    n, m = 1000, 100
+    t, p = rand_records(rng, n, m), rand_records(rng, n, m)
+    np_ = L.lib.pf_nibble_pitch(m)
+    raw_t = np.full(n * np_ + 192, 0xEE, np.uint8)
+    raw_p = np.full(n * np_ + 192, 0xEE, np.uint8)
+    base_t = (-raw_t.ctypes.data) % 64 + offset
+    base_p = (-raw_p.ctypes.data) % 64 + offset
+    err = L.PfError()
+    st = L.lib.pf_host_pack_nibbles(t.ctypes.data_as(C.c_void_p), p.ctypes.data_as(C.c_void_p), m,
+                                    n, m, C.c_void_p(raw_t.ctypes.data + base_t),
+                                    C.c_void_p(raw_p.ctypes.data + base_p), 1, C.byref(err))
+    assert st == 0
+    assert (raw_t[base_t:base_t + n * np_].reshape(n, np_) == ref_nibbles(t)).all()
+    assert (raw_p[base_p:base_p + n * np_].reshape(n, np_) == ref_nibbles(p)).all()
+    assert (raw_t[:base_t] == 0xEE).all() and (raw_t[base_t + n * np_:] == 0xEE).all()
+    assert (raw_p[:base_p] == 0xEE).all() and (raw_p[base_p + n * np_:] == 0xEE).all()
