@@ -70,6 +70,16 @@ class Oracle:
         lib.so_banded_edit_distance.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, C.c_uint32]
         lib.so_banded_edit_distance.restype = C.c_int32
         lib.so_set_variant.argtypes = [C.c_int]
+        lib.so_magnet_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t,
+                                        C.c_uint32, C.c_uint, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.POINTER(_SoError)]
+        lib.so_magnet_one.argtypes = [C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t, C.c_uint32,
+                                      C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_int)]
+        lib.so_recover_subsequences.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t, C.c_uint32,
+                                                C.c_uint32, C.c_void_p, C.c_void_p]
+        lib.so_recover_subsequences.restype = C.c_size_t
+        lib.so_longest_zero_run.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t,
+                                            C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
         self.lib = lib
 
     def set_variant(self, v: int):
@@ -122,6 +132,53 @@ class Oracle:
     def banded_edit_distance(self, pattern: bytes, text: bytes, e: int) -> int:
         return self.lib.so_banded_edit_distance(pattern, text, len(text), e)
 
+    # ---- MAGNET (magnet.cpp) ----
+    def magnet_batch(self, text, pattern, e, threads=None, estimates=True, bits=False):
+        """Returns (accept_bitmap u32[ceil(n/32)], estimates u32[n] | None, bits u64[n, W64] | None)."""
+        text, pattern = _records(text, pattern)
+        n, m = text.shape
+        threads = threads or os.cpu_count() or 1
+        acc = np.zeros((n + 31) // 32, np.uint32)
+        est = np.zeros(n, np.uint32) if estimates else None
+        bv = np.zeros((n, (m + 63) // 64), np.uint64) if bits else None
+        err = _SoError()
+        st = self.lib.so_magnet_batch(_ptr(text), _ptr(pattern), m, n, m, e, threads, _ptr(acc),
+                                      _ptr(est), _ptr(bv), C.byref(err))
+        if st:
+            raise OracleError(st, err.pair, err.field, err.position, err.byte)
+        return acc, est, bv
+
+    def magnet_one(self, pattern: str, text: str, e: int):
+        """magnet_filter(seq(pattern), seq(text), e) -> (accept, estimate, bits str)."""
+        pb, tb = pattern.encode(), text.encode()
+        bits = np.zeros(max(len(tb), 1), np.uint8)
+        est, acc = C.c_uint32(), C.c_int()
+        st = self.lib.so_magnet_one(pb, len(pb), tb, len(tb), e, _ptr(bits), C.byref(est),
+                                    C.byref(acc))
+        if st:
+            raise OracleError(st)
+        return bool(acc.value), est.value, "".join("1" if b else "0" for b in bits[:len(tb)])
+
+    def recover(self, pattern: str, text: str, e: int, budget: int):
+        """recover_subsequences(map(pattern, text, e), budget) -> ([(d, start, len, lo, hi)], bits str)."""
+        m = len(text)
+        bv = np.zeros(m, np.uint8)
+        class _X(C.Structure):
+            _fields_ = [("diagonal", C.c_int), ("start", C.c_size_t), ("len", C.c_size_t),
+                        ("lo", C.c_size_t), ("hi", C.c_size_t)]
+        xs = (_X * max(budget, 1))()
+        k = self.lib.so_recover_subsequences(pattern.encode(), text.encode(), m, e, budget,
+                                             _ptr(bv), C.cast(xs, C.c_void_p))
+        ext = [(xs[i].diagonal, xs[i].start, xs[i].len, xs[i].lo, xs[i].hi) for i in range(k)]
+        return ext, "".join("1" if b else "0" for b in bv)
+
+    def longest_zero_run(self, bits: str, lo: int, hi: int):
+        b = np.frombuffer(bits.encode(), np.uint8) - ord("0")
+        b = np.ascontiguousarray(b.astype(np.uint8))
+        st, ln = C.c_size_t(), C.c_size_t()
+        self.lib.so_longest_zero_run(_ptr(b), len(bits), lo, hi, C.byref(st), C.byref(ln))
+        return st.value, ln.value
+
 
 class Reference:
     """The unmodified reference library (oracle/_ref/libprefilter_ref.so)."""
@@ -145,6 +202,12 @@ class Reference:
         lib.ref_hardware_concurrency.restype = C.c_uint
         lib.ref_load_pairs_tsv.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t),
                                            C.POINTER(C.c_size_t), C.c_char_p, C.c_size_t]
+        lib.ref_magnet_one.argtypes = [C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t, C.c_uint32,
+                                       C.POINTER(C.c_int), C.POINTER(C.c_uint32), C.c_char_p,
+                                       C.c_int64, C.c_void_p, C.c_size_t,
+                                       C.POINTER(C.c_size_t), C.c_char_p]
+        lib.ref_longest_zero_run.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t, C.c_size_t,
+                                             C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
         self.lib = lib
 
     def load_pairs(self, data: bytes):
@@ -186,6 +249,39 @@ class Reference:
             return packed.shouji(e, width, threads, estimates, bits)
         finally:
             packed.free()
+
+    def magnet_batch(self, text, pattern, e, threads=None):
+        packed = self.pack(text, pattern)
+        try:
+            return packed.magnet(e, threads)
+        finally:
+            packed.free()
+
+    def magnet_one(self, pattern: str, text: str, e: int, budget: int | None = None):
+        """magnet_filter -> (accept, estimate, bits str); with budget also
+        recover_subsequences(map, budget) -> ([(d, start, len, lo, hi)], bits str)."""
+        pb, tb = pattern.encode(), text.encode()
+        acc, est = C.c_int(), C.c_uint32()
+        buf = C.create_string_buffer(len(tb) + 1)
+        rbuf = C.create_string_buffer(len(tb) + 1)
+        nmax = max(budget or 0, 1)
+        ext = (C.c_int64 * (5 * nmax))()
+        n_ext = C.c_size_t()
+        st = self.lib.ref_magnet_one(pb, len(pb), tb, len(tb), e, C.byref(acc), C.byref(est), buf,
+                                     -1 if budget is None else budget, ext, nmax, C.byref(n_ext),
+                                     rbuf)
+        if st:
+            raise OracleError(st)
+        out = (bool(acc.value), est.value, buf.value.decode())
+        if budget is None:
+            return out
+        xs = [tuple(int(v) for v in ext[5 * k:5 * k + 5]) for k in range(min(n_ext.value, nmax))]
+        return out, (xs, rbuf.value.decode())
+
+    def longest_zero_run(self, bits: str, lo: int, hi: int):
+        st, ln = C.c_size_t(), C.c_size_t()
+        self.lib.ref_longest_zero_run(bits.encode(), len(bits), lo, hi, C.byref(st), C.byref(ln))
+        return st.value, ln.value
 
     def shouji_one(self, pattern: str, text: str, e: int, width: int = 4):
         pb, tb = pattern.encode(), text.encode()

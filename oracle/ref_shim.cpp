@@ -267,4 +267,56 @@ int ref_load_pairs_tsv(const char* data, std::size_t len, std::size_t* n, std::s
     }
 }
 
+// magnet_filter (proj/src/magnet.cpp:77-87) for one pair, plus the extraction
+// list of recover_subsequences(map, budget) (:70-75) when budget is given:
+// ext receives (diagonal, start, len, lo, hi) per extraction (up to max_ext).
+int ref_magnet_one(const char* pattern, std::size_t pattern_len, const char* text,
+                   std::size_t text_len, std::uint32_t e, int* accept, std::uint32_t* estimate,
+                   char* bits_string, std::int64_t budget, std::int64_t* ext, std::size_t max_ext,
+                   std::size_t* n_ext, char* rec_bits_string) {
+    try {
+        const auto p = prefilter::packed_sequence::from_string({pattern, pattern_len});
+        const auto t = prefilter::packed_sequence::from_string({text, text_len});
+        const auto d = prefilter::magnet_filter(p, t, e);
+        *accept = d.accept ? 1 : 0;
+        *estimate = d.edit_estimate;
+        if (bits_string) {
+            const std::string s = d.bits.to_string();
+            std::memcpy(bits_string, s.data(), s.size());
+            bits_string[s.size()] = '\0';
+        }
+        if (budget >= 0 && n_ext) {
+            const auto rec = prefilter::recover_subsequences(
+                prefilter::neighborhood_map(p, t, e), static_cast<std::uint32_t>(budget));
+            *n_ext = rec.extractions.size();
+            for (std::size_t k = 0; k < rec.extractions.size() && k < max_ext; ++k) {
+                const auto& x = rec.extractions[k];
+                ext[5 * k + 0] = x.diagonal;
+                ext[5 * k + 1] = static_cast<std::int64_t>(x.start);
+                ext[5 * k + 2] = static_cast<std::int64_t>(x.len);
+                ext[5 * k + 3] = static_cast<std::int64_t>(x.lo);
+                ext[5 * k + 4] = static_cast<std::int64_t>(x.hi);
+            }
+            if (rec_bits_string) {
+                const std::string s = rec.bits.to_string();
+                std::memcpy(rec_bits_string, s.data(), s.size());
+                rec_bits_string[s.size()] = '\0';
+            }
+        }
+        return kOk;
+    } catch (...) {
+        return map_exception(std::current_exception(), nullptr);
+    }
+}
+
+// longest_zero_run (proj/src/magnet.cpp:9-22) on a '0'/'1' string.
+void ref_longest_zero_run(const char* bits, std::size_t nbits, std::size_t lo, std::size_t hi,
+                          std::size_t* start, std::size_t* len) {
+    prefilter::bitvector bv(nbits);
+    for (std::size_t i = 0; i < nbits; ++i) bv.set(i, bits[i] == '1');
+    const auto r = prefilter::longest_zero_run(bv, lo, hi);
+    *start = r.start;
+    *len = r.len;
+}
+
 }  // extern "C"

@@ -394,3 +394,209 @@ int32_t so_banded_edit_distance(const char* a, const char* b, size_t m, uint32_t
     free(cur);
     return d <= e ? (int32_t)d : -1;
 }
+
+/* ---- MAGNET (proj/src/magnet.cpp) --------------------------------------- */
+
+/* longest_zero_run — proj/src/magnet.cpp:9-22: the longest run of zeros in
+ * bits[lo..hi] (inclusive, hi clipped to m-1); the earliest wins ties; an
+ * inverted or empty range gives len 0 with start = lo. */
+void so_longest_zero_run(const uint8_t* bits, size_t m, size_t lo, size_t hi, size_t* start,
+                         size_t* len) {
+    size_t best_start = lo, best_len = 0, run_start = 0, run_len = 0;
+    const size_t end = hi < m ? hi : m - 1;
+    for (size_t i = lo; i <= end && lo <= hi; ++i) {
+        if (!bits[i]) {
+            if (run_len == 0) run_start = i;
+            if (++run_len > best_len) {
+                best_start = run_start;
+                best_len = run_len;
+            }
+        } else {
+            run_len = 0;
+        }
+    }
+    *start = best_start;
+    *len = best_len;
+}
+
+typedef struct {
+    int diagonal;
+    size_t start, len, lo, hi;
+} so_extraction;
+
+typedef struct {
+    uint8_t* map; /* (2e+1) x m, row d+e, mutated by column masking */
+    size_t m;
+    uint32_t e;
+    uint32_t budget;
+    uint8_t* bv;
+    so_extraction* out;
+    size_t nout;
+} so_magnet_state;
+
+/* exen — proj/src/magnet.cpp:29-66: nominate each diagonal's longest run in
+ * the active range in the order 0, -1, +1, -2, +2, ... (only a strictly longer
+ * run displaces the incumbent), extract the winner (clear its bits in bv),
+ * mask the run plus one flanking column on every diagonal
+ * (neighborhood_map::mask_columns, neighborhood.cpp:88-91), then recurse into
+ * the left range, then the right range, on the shared budget. */
+static void so_exen(so_magnet_state* s, int64_t lo, int64_t hi) {
+    if (s->budget == 0 || lo > hi) return;
+    const size_t clo = (size_t)(lo < 0 ? 0 : lo);
+    const size_t chi = (size_t)(hi >= (int64_t)s->m ? (int64_t)s->m - 1 : hi);
+    if (clo > chi) return;
+    const int e = (int)s->e;
+    size_t best_start = 0, best_len = 0;
+    int best_d = 0;
+    for (int step = 0; step <= e; ++step) {
+        for (int k = 0; k < 2; ++k) {
+            const int d = k == 0 ? -step : step;
+            size_t st, ln;
+            so_longest_zero_run(s->map + (size_t)(d + e) * s->m, s->m, clo, chi, &st, &ln);
+            if (ln > best_len) {
+                best_start = st;
+                best_len = ln;
+                best_d = d;
+            }
+            if (step == 0) break;
+        }
+    }
+    if (best_len == 0) return;
+    --s->budget;
+    for (size_t i = best_start; i < best_start + best_len; ++i) s->bv[i] = 0;
+    if (s->out) {
+        so_extraction x = {best_d, best_start, best_len, clo, chi};
+        s->out[s->nout] = x;
+    }
+    ++s->nout;
+    /* mask_columns(lo', hi') sets columns lo'..hi' (inclusive) to 1 on every diagonal */
+    const size_t mlo = best_start > 0 ? best_start - 1 : 0;
+    const size_t mhi = best_start + best_len;
+    if (mlo <= mhi && mlo < s->m)
+        for (int d = -e; d <= e; ++d)
+            for (size_t i = mlo; i <= mhi && i < s->m; ++i) s->map[(size_t)(d + e) * s->m + i] = 1;
+    so_exen(s, lo, (int64_t)best_start - 2);
+    so_exen(s, (int64_t)(best_start + best_len) + 1, hi);
+}
+
+/* recover_subsequences — proj/src/magnet.cpp:70-75 (on a copy of the map). bv
+ * (m bytes) starts all ones; out (nullable, >= budget entries) receives the
+ * extractions in order. Returns the number of extractions. */
+size_t so_recover_subsequences(const char* pattern, const char* text, size_t m, uint32_t e,
+                               uint32_t budget, uint8_t* bv, so_extraction* out) {
+    uint8_t* map = (uint8_t*)malloc((2 * (size_t)e + 1) * m);
+    so_neighborhood(pattern, text, m, e, map);
+    memset(bv, 1, m);
+    so_magnet_state s = {map, m, e, budget, bv, out, 0};
+    so_exen(&s, 0, (int64_t)m - 1);
+    free(map);
+    return s.nout;
+}
+
+/* magnet_filter — proj/src/magnet.cpp:77-87: length check, e >= m accepts
+ * with estimate 0 and all-zero bits, else e+1 extractions; estimate =
+ * popcount(bv), accept = estimate <= e. */
+int so_magnet_one(const char* pattern, size_t pattern_len, const char* text, size_t text_len,
+                  uint32_t e, uint8_t* bits_out, uint32_t* estimate, int* accept) {
+    if (pattern_len != text_len) return SO_LENGTH_MISMATCH;
+    const size_t m = text_len;
+    if ((size_t)e >= m) {
+        if (bits_out) memset(bits_out, 0, m);
+        *estimate = 0;
+        *accept = 1;
+        return SO_OK;
+    }
+    uint8_t* bv = bits_out ? bits_out : (uint8_t*)malloc(m);
+    so_recover_subsequences(pattern, text, m, e, e + 1, bv, NULL);
+    uint32_t ones = 0;
+    for (size_t j = 0; j < m; ++j) ones += bv[j];
+    *estimate = ones;
+    *accept = ones <= e;
+    if (!bits_out) free(bv);
+    return SO_OK;
+}
+
+typedef struct {
+    const char* text;
+    const char* pattern;
+    size_t stride, m, begin, end;
+    uint32_t e;
+    uint8_t* acc;
+    uint32_t* estimates;
+    uint64_t* bits;
+    size_t words_per_pair;
+} so_mjob;
+
+static void* so_magnet_worker(void* arg) {
+    so_mjob* job = (so_mjob*)arg;
+    const size_t m = job->m;
+    uint8_t* bv = (uint8_t*)malloc(m);
+    for (size_t i = job->begin; i < job->end; ++i) {
+        uint32_t est;
+        int accept;
+        so_magnet_one(job->pattern + i * job->stride, m, job->text + i * job->stride, m, job->e,
+                      bv, &est, &accept);
+        job->acc[i] = (uint8_t)accept;
+        if (job->estimates) job->estimates[i] = est;
+        if (job->bits) {
+            uint64_t* dst = job->bits + i * job->words_per_pair;
+            memset(dst, 0, job->words_per_pair * sizeof(uint64_t));
+            for (size_t j = 0; j < m; ++j)
+                if (bv[j]) dst[j >> 6] |= (uint64_t)1 << (j & 63);
+        }
+    }
+    free(bv);
+    return NULL;
+}
+
+/* Batch MAGNET over ASCII records, as run_filter(magnet) is driven by the
+ * reference's callers (evaluate.cpp:13-48): validation of every pair first
+ * (text then pattern, first error wins), then magnet_filter per pair. */
+int so_magnet_batch(const char* text, const char* pattern, size_t stride, size_t n, size_t m,
+                    uint32_t e, unsigned threads, uint32_t* accept_bitmap, uint32_t* estimates,
+                    uint64_t* bits, so_error* err) {
+    if (err) memset(err, 0, sizeof(*err));
+    if (n == 0) return SO_OK;
+    for (size_t i = 0; i < n; ++i) {
+        for (int field = 0; field < 2; ++field) {
+            uint64_t pos = 0;
+            int byte = 0;
+            const int st = so_validate((field == 0 ? text : pattern) + i * stride, m, &pos, &byte);
+            if (st != SO_OK) {
+                if (err) {
+                    err->code = st;
+                    err->pair = i;
+                    err->field = field;
+                    err->position = pos;
+                    err->byte = byte;
+                }
+                return st;
+            }
+        }
+    }
+    const size_t words_per_pair = (m + 63) / 64;
+    if (accept_bitmap) memset(accept_bitmap, 0, ((n + 31) / 32) * sizeof(uint32_t));
+    uint8_t* acc = (uint8_t*)calloc(n, 1);
+    if (threads < 1) threads = 1;
+    if (threads > n) threads = (unsigned)n;
+    pthread_t* tids = (pthread_t*)malloc(threads * sizeof(pthread_t));
+    so_mjob* jobs = (so_mjob*)malloc(threads * sizeof(so_mjob));
+    for (unsigned t = 0; t < threads; ++t) {
+        so_mjob j = {text, pattern, stride, m, n * t / threads, n * (t + 1) / threads, e,
+                     acc, estimates, bits, words_per_pair};
+        jobs[t] = j;
+        if (threads == 1)
+            so_magnet_worker(&jobs[t]);
+        else
+            pthread_create(&tids[t], NULL, so_magnet_worker, &jobs[t]);
+    }
+    if (threads > 1)
+        for (unsigned t = 0; t < threads; ++t) pthread_join(tids[t], NULL);
+    if (accept_bitmap)
+        for (size_t i = 0; i < n; ++i)
+            if (acc[i]) accept_bitmap[i / 32] |= 1u << (i % 32);
+    free(jobs);
+    free(tids);
+    free(acc);
+    return SO_OK;
+}
