@@ -169,6 +169,27 @@ int pf_shouji_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, c
                          size_t text_len, uint32_t e, uint32_t width, int* accept,
                          uint32_t* estimate, uint64_t* bits, pf_error* err);
 
+/* ---- MAGNET (proj/src/magnet.cpp) --------------------------
+ * magnet_filter(pattern, text, e) (magnet.cpp:77-87) over a batch: e+1
+ * extract-and-encapsulate steps over the 2e+1 diagonals; estimate =
+ * popcount(bits), accept = estimate <= e; e >= m accepts with estimate 0 and
+ * all-zero bits. Same validation, error order, outputs and sharding as
+ * pf_shouji_filter_batch (no width). One GPU thread per pair; m <= 512.
+ * Replaces run_filter(filter_algo::magnet, ...) (evaluate.cpp:13-21). */
+int pf_magnet_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t stride,
+                           size_t n, uint32_t m, uint32_t e, uint32_t* accept_bitmap,
+                           uint32_t* estimates, uint64_t* bits, pf_error* err);
+/* Device-resident records (same layout rules as pf_shouji_filter_device),
+ * synchronous validation, results stream-ordered on `stream`. */
+int pf_magnet_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                            size_t pitch, size_t n, uint32_t m, uint32_t e,
+                            uint32_t* d_accept_bitmap, uint32_t* d_estimates, uint64_t* d_bits,
+                            void* stream, pf_error* err);
+/* Per-pair magnet_filter(pattern, text, e) (a batch of one). */
+int pf_magnet_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, const char* text,
+                         size_t text_len, uint32_t e, int* accept, uint32_t* estimate,
+                         uint64_t* bits, pf_error* err);
+
 /* Pinned host allocation helpers (cudaHostAlloc on the ctx's first device). */
 void* pf_host_alloc(size_t bytes);
 void pf_host_free(void* p);

@@ -35,6 +35,9 @@ from .api import (  # noqa: F401
     shouji_filter_device,
     shouji_filter_device_async,
     int_peak,
+    magnet_filter,
+    magnet_filter_batch,
+    magnet_filter_device,
     nibble_pitch,
     host_pack_nibbles,
     shouji_filter_nibbles_device,

@@ -35,7 +35,8 @@ EXPORTED = [
     "pf_dataset_size", "pf_dataset_length", "pf_dataset_text", "pf_dataset_pattern",
     "pf_dataset_source", "pf_dataset_write_tsv", "pf_dataset_free", "pf_banded_edit_distance_batch",
     "pf_nibble_pitch", "pf_host_pack_nibbles", "pf_shouji_filter_nibbles_device",
-    "pf_transfer_bytes",
+    "pf_transfer_bytes", "pf_magnet_filter_batch", "pf_magnet_filter_device",
+    "pf_magnet_filter_one",
 ]
 
 
@@ -98,6 +99,13 @@ def _bind(lib):
                                                     C.POINTER(PfError)]),
         "pf_nibble_pitch": (_sz, [_u32]),
         "pf_transfer_bytes": (None, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+        "pf_magnet_filter_batch": (C.c_int, [_vp, _vp, _vp, _sz, _sz, _u32, _u32, _vp, _vp, _vp,
+                                             C.POINTER(PfError)]),
+        "pf_magnet_filter_device": (C.c_int, [_vp, _vp, _vp, _sz, _sz, _u32, _u32, _vp, _vp, _vp,
+                                              _vp, C.POINTER(PfError)]),
+        "pf_magnet_filter_one": (C.c_int, [_vp, C.c_char_p, _sz, C.c_char_p, _sz, _u32,
+                                           C.POINTER(C.c_int), C.POINTER(_u32), _vp,
+                                           C.POINTER(PfError)]),
         "pf_host_pack_nibbles": (C.c_int, [_vp, _vp, _sz, _sz, _u32, _vp, _vp, C.c_int,
                                            C.POINTER(PfError)]),
         "pf_shouji_filter_nibbles_device": (C.c_int, [_vp, _vp, _vp, _sz, _u32, _u32, _u32, _vp,

@@ -300,12 +300,32 @@ def shouji_filter(pattern: packed_sequence, text: packed_sequence, e: int,
     return filter_decision(bool(acc.value), int(est.value), bitvector(nbits, words=words))
 
 
+def magnet_filter(pattern: packed_sequence, text: packed_sequence, e: int,
+                  ctx: Context | None = None) -> filter_decision:
+    """magnet_filter(pattern=read, text=reference segment, e) — magnet.hpp:55-57.
+
+    Raises length_mismatch_error (magnet.cpp:79-80); e >= m accepts with estimate 0.
+    """
+    ctx = ctx or default_context()
+    pb, tb = pattern.ascii(), text.ascii()
+    acc, est = C.c_int(), C.c_uint32()
+    nbits = len(tb)
+    words = np.zeros(max((nbits + 63) // 64, 1), np.uint64)
+    err = L.PfError()
+    st = L.lib.pf_magnet_filter_one(ctx.handle, pb, len(pb), tb, len(tb), int(e), C.byref(acc),
+                                    C.byref(est), words.ctypes.data_as(C.c_void_p), C.byref(err))
+    _raise(st, err)
+    return filter_decision(bool(acc.value), int(est.value), bitvector(nbits, words=words))
+
+
 def run_filter(algo: str, pattern: packed_sequence, text: packed_sequence, e: int,
                width: int = default_window_width) -> filter_decision:
-    """run_filter (evaluate.cpp:13-21) for the path this framework accelerates."""
-    if algo != "shouji":
-        raise invalid_parameters_error(f"filter '{algo}' is outside this framework's scope")
-    return shouji_filter(pattern, text, e, width)
+    """run_filter (evaluate.cpp:13-21): "shouji" or "magnet" (width is Shouji's only)."""
+    if algo == "shouji":
+        return shouji_filter(pattern, text, e, width)
+    if algo == "magnet":
+        return magnet_filter(pattern, text, e)
+    raise invalid_parameters_error(f"unknown filter '{algo}'")
 
 
 def _as_records(x, m=None):
@@ -338,6 +358,39 @@ def shouji_filter_batch(text, pattern, e: int, width: int = default_window_width
                                       int(width), ptr(acc), ptr(est), ptr(bv), C.byref(err))
     _raise(st, err)
     return acc, est, bv
+
+
+def magnet_filter_batch(text, pattern, e: int, m: int | None = None, estimates: bool = False,
+                        bits: bool = False, ctx: Context | None = None):
+    """MAGNET over N pairs of host ASCII records (same layout and returns as
+    shouji_filter_batch)."""
+    ctx = ctx or default_context()
+    text = _as_records(text)
+    pattern = _as_records(pattern)
+    if text.shape != pattern.shape:
+        raise length_mismatch_error("text and pattern record arrays differ in shape")
+    n, stride = text.shape
+    m = stride if m is None else int(m)
+    acc = np.zeros((n + 31) // 32, np.uint32)
+    est = np.zeros(n, np.uint32) if estimates else None
+    bv = np.zeros((n, (m + 63) // 64), np.uint64) if bits else None
+    err = L.PfError()
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p) if a is not None else None  # noqa: E731
+    st = L.lib.pf_magnet_filter_batch(ctx.handle, ptr(text), ptr(pattern), stride, n, m, int(e),
+                                      ptr(acc), ptr(est), ptr(bv), C.byref(err))
+    _raise(st, err)
+    return acc, est, bv
+
+
+def magnet_filter_device(d_text: int, d_pattern: int, pitch: int, n: int, m: int, e: int,
+                         d_accept: int, d_estimates: int | None = None, d_bits: int | None = None,
+                         stream: int | None = None, ctx: Context | None = None) -> None:
+    """MAGNET over device-resident records (raw device pointers)."""
+    ctx = ctx or default_context()
+    err = L.PfError()
+    st = L.lib.pf_magnet_filter_device(ctx.handle, d_text, d_pattern, pitch, n, m, int(e), d_accept,
+                                       d_estimates, d_bits, stream, C.byref(err))
+    _raise(st, err)
 
 
 def shouji_filter_device(d_text: int, d_pattern: int, pitch: int, n: int, m: int, e: int,

@@ -222,7 +222,7 @@ struct ShardResult {
 void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern, size_t stride,
                     size_t p0, size_t p1, uint32_t m, uint32_t e, uint32_t width,
                     uint32_t* accept_bitmap, uint32_t* estimates, uint64_t* bits, int32_t* dist,
-                    ShardResult* res) {
+                    bool magnet, ShardResult* res) {
     pf_error* err = &res->err;
     auto fail = [&](int st) { res->status = st; };
     const size_t n = p1 - p0;
@@ -239,7 +239,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         return false;
     };
     const int hp_mode = host_pack_mode();
-    const bool host_pack = hp_mode != 0 && !dist && e < m && width >= 3 && width <= 8 && !bits &&
+    const bool host_pack = hp_mode != 0 && !dist && !magnet && e < m && width >= 3 && width <= 8 && !bits &&
                            sb::nibble_pack_fits(static_cast<int>(m)) &&
                            (hp_mode == 1 || static_cast<long long>(n) >= kHostPackMin);
     if (!host_pack) {
@@ -252,7 +252,8 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     const size_t wpp = (m + 63) / 64;
     if (bits) {
         if (!cu(grow(d.d_bits, d.bits_words, n * wpp), "alloc bits")) return;
-        if (!cu(grow(d.d_outplanes, d.outplanes_words, size_t(m) * ngroups), "alloc tally planes"))
+        if (!magnet &&
+            !cu(grow(d.d_outplanes, d.outplanes_words, size_t(m) * ngroups), "alloc tally planes"))
             return;
     }
     if (!d.d_flag) {
@@ -429,13 +430,13 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     a.width = width;
     a.accept = d.d_accept;
     a.estimates = estimates ? d.d_est : nullptr;
-    a.outplanes = bits ? d.d_outplanes : nullptr;
+    a.outplanes = bits && !magnet ? d.d_outplanes : nullptr;
     a.err_flag = d.d_flag;
     a.planes = d.d_scratch;
     a.planes_words = d.scratch_words;
     const bool short_circuit = e >= m;
-    const bool bad_width = !dist && (width < 3 || width > 8);
-    if (short_circuit || bad_width || dist) {
+    const bool bad_width = !dist && !magnet && (width < 3 || width > 8);
+    if (short_circuit || bad_width || dist || magnet) {
         if (!cu(sb::launch_validate(a, d.stream), "validate")) return;
     } else {
         if (!cu(launch_any(d, a, d.stream), "filter kernel")) return;
@@ -477,6 +478,12 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         if (!cu(sb::launch_accept_all(a.n, a.m, d.d_accept, estimates ? d.d_est : nullptr,
                                       bits ? d.d_bits : nullptr, d.stream),
                 "accept_all"))
+            return;
+    } else if (magnet) {
+        if (!cu(sb::launch_magnet(d.d_text, d.d_pattern, pitch, a.n, a.m, static_cast<int>(e),
+                                  d.d_accept, estimates ? d.d_est : nullptr,
+                                  bits ? d.d_bits : nullptr, d.stream),
+                "magnet kernel"))
             return;
     } else if (bits) {
         if (!cu(sb::launch_bits_transpose(d.d_outplanes, a.n, a.m, d.d_bits, d.stream), "bits"))
@@ -682,7 +689,7 @@ namespace {
 
 int run_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t stride, size_t n,
               uint32_t m, uint32_t e, uint32_t width, uint32_t* accept_bitmap, uint32_t* estimates,
-              uint64_t* bits, int32_t* dist, pf_error* err) {
+              uint64_t* bits, int32_t* dist, pf_error* err, bool magnet = false) {
     if (err) std::memset(err, 0, sizeof(*err));
     if (!ctx) return PF_ERR_NULL_ARGUMENT;
     if (n == 0) return PF_OK;
@@ -691,9 +698,12 @@ int run_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t s
         set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
         return PF_ERR_EMPTY_SEQUENCE;
     }
-    if (stride < m || m >= (1u << 24) || (dist && m > 1024)) {
+    if (stride < m || m >= (1u << 24) || (dist && m > 1024) ||
+        (magnet && e < m && !sb::magnet_supported(static_cast<int>(m)))) {
         set_err(err, PF_ERR_INVALID_PARAMETERS,
-                dist ? "stride < m or m > 1024 (edit distance)" : "stride < m or m >= 2^24");
+                dist     ? "stride < m or m > 1024 (edit distance)"
+                : magnet ? "stride < m or m > 512 (MAGNET)"
+                         : "stride < m or m >= 2^24");
         return PF_ERR_INVALID_PARAMETERS;
     }
     std::lock_guard<std::mutex> lock(ctx->mu);
@@ -705,13 +715,13 @@ int run_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t s
     std::vector<ShardResult> res(nd);
     if (nd == 1) {
         run_host_shard(ctx->devs[0], text, pattern, stride, bounds[0], bounds[1], m, e, width,
-                       accept_bitmap, estimates, bits, dist, &res[0]);
+                       accept_bitmap, estimates, bits, dist, magnet, &res[0]);
     } else {
         std::vector<std::thread> pool;
         for (size_t t = 0; t < nd; ++t)
             pool.emplace_back(run_host_shard, std::ref(ctx->devs[t]), text, pattern, stride,
                               bounds[t], bounds[t + 1], m, e, width, accept_bitmap, estimates, bits,
-                              dist, &res[t]);
+                              dist, magnet, &res[t]);
         for (auto& th : pool) th.join();
     }
     // First failure in pair order wins (illegal characters are located per
@@ -723,7 +733,7 @@ int run_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t s
             return res[t].status;
         }
     }
-    if (!dist && (width < 3 || width > 8)) {  // window_zero_table ctor (shouji.cpp:9-15)
+    if (!dist && !magnet && (width < 3 || width > 8)) {  // window_zero_table ctor (shouji.cpp:9-15)
         set_err(err, PF_ERR_INVALID_PARAMETERS, "window width must be in [3, 8]");
         return PF_ERR_INVALID_PARAMETERS;
     }
@@ -740,6 +750,71 @@ int pf_shouji_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* patt
                            pf_error* err) {
     return run_batch(ctx, text, pattern, stride, n, m, e, width, accept_bitmap, estimates, bits,
                      nullptr, err);
+}
+
+int pf_magnet_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t stride,
+                           size_t n, uint32_t m, uint32_t e, uint32_t* accept_bitmap,
+                           uint32_t* estimates, uint64_t* bits, pf_error* err) {
+    return run_batch(ctx, text, pattern, stride, n, m, e, 4, accept_bitmap, estimates, bits,
+                     nullptr, err, true);
+}
+
+int pf_magnet_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                            size_t pitch, size_t n, uint32_t m, uint32_t e,
+                            uint32_t* d_accept_bitmap, uint32_t* d_estimates, uint64_t* d_bits,
+                            void* stream, pf_error* err) {
+    if (err) std::memset(err, 0, sizeof(*err));
+    if (!ctx) return PF_ERR_NULL_ARGUMENT;
+    if (n == 0) return PF_OK;
+    if (!d_text || !d_pattern || !d_accept_bitmap) return PF_ERR_NULL_ARGUMENT;
+    if (m == 0) {
+        set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
+        return PF_ERR_EMPTY_SEQUENCE;
+    }
+    if (pitch % 4 != 0 || pitch < m ||
+        (reinterpret_cast<uintptr_t>(d_text) | reinterpret_cast<uintptr_t>(d_pattern)) % 16 != 0 ||
+        m >= (1u << 24) || (e < m && !sb::magnet_supported(static_cast<int>(m)))) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS,
+                "device records need 16-byte aligned bases, pitch % 4 == 0, pitch >= m, m <= 512");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceState& d = ctx->devs[0];
+    PF_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!d.d_flag) {
+        PF_CUDA(cudaMalloc(&d.d_flag, sizeof(uint32_t)));
+        PF_CUDA(cudaMalloc(&d.d_key, sizeof(unsigned long long)));
+    }
+    PF_CUDA(cudaMemsetAsync(d.d_flag, 0, sizeof(uint32_t), s));
+    sb::FilterArgs a{};
+    a.text = d_text;
+    a.pattern = d_pattern;
+    a.pitch = pitch;
+    a.n = static_cast<long long>(n);
+    a.m = static_cast<int>(m);
+    a.e = e;
+    a.err_flag = d.d_flag;
+    PF_CUDA(sb::launch_validate(a, s));
+    uint32_t flag = 0;
+    PF_CUDA(cudaMemcpyAsync(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
+    PF_CUDA(cudaStreamSynchronize(s));
+    if (flag) {
+        const unsigned long long init = ~0ull;
+        PF_CUDA(cudaMemcpy(d.d_key, &init, sizeof(init), cudaMemcpyHostToDevice));
+        PF_CUDA(sb::launch_locate(d_text, d_pattern, pitch, a.n, a.m, d.d_key, s));
+        unsigned long long key = 0;
+        PF_CUDA(cudaMemcpyAsync(&key, d.d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
+        PF_CUDA(cudaStreamSynchronize(s));
+        decode_illegal(key, 0, d_text, d_pattern, pitch, false, err);
+        return PF_ERR_ILLEGAL_CHARACTER;
+    }
+    if (e >= m)
+        PF_CUDA(sb::launch_accept_all(a.n, a.m, d_accept_bitmap, d_estimates, d_bits, s));
+    else
+        PF_CUDA(sb::launch_magnet(d_text, d_pattern, pitch, a.n, a.m, static_cast<int>(e),
+                                  d_accept_bitmap, d_estimates, d_bits, s));
+    return PF_OK;
 }
 
 int pf_banded_edit_distance_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern,
@@ -867,9 +942,19 @@ int pf_int_peak(pf_ctx* ctx, int op, double* ops_per_second) {
     return PF_OK;
 }
 
-int pf_shouji_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, const char* text,
-                         size_t text_len, uint32_t e, uint32_t width, int* accept,
-                         uint32_t* estimate, uint64_t* bits, pf_error* err) {
+}  // extern "C"
+
+namespace {
+
+// Per-pair entry points (shouji_filter / magnet_filter signatures): the
+// caller's packed_sequence objects would have been built (and validated)
+// before the filter runs — pattern first, then text — then the filter checks
+// lengths (shouji.cpp:44-45, magnet.cpp:79-80) and, for Shouji, the width
+// (shouji.cpp:47, before the e >= m short-circuit). The pair then runs as a
+// batch of one on the device.
+int filter_one(pf_ctx* ctx, bool magnet, const char* pattern, size_t pattern_len,
+               const char* text, size_t text_len, uint32_t e, uint32_t width, int* accept,
+               uint32_t* estimate, uint64_t* bits, pf_error* err) {
     if (err) std::memset(err, 0, sizeof(*err));
     if (!ctx || !accept || !estimate) return PF_ERR_NULL_ARGUMENT;
     if (pattern_len == 0 || text_len == 0) {
@@ -877,8 +962,6 @@ int pf_shouji_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, c
         return PF_ERR_EMPTY_SEQUENCE;
     }
     if (!pattern || !text) return PF_ERR_NULL_ARGUMENT;
-    // The caller's packed_sequence objects would have been built (and
-    // validated) before shouji_filter runs; pattern first, then text.
     for (int field = 0; field < 2; ++field) {
         const char* s = field == 0 ? pattern : text;
         const size_t len = field == 0 ? pattern_len : text_len;
@@ -898,22 +981,43 @@ int pf_shouji_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, c
             }
         }
     }
-    if (pattern_len != text_len) {  // shouji.cpp:44-45
+    if (pattern_len != text_len) {
         set_err(err, PF_ERR_LENGTH_MISMATCH, "length mismatch");
         return PF_ERR_LENGTH_MISMATCH;
     }
-    if (width < 3 || width > 8) {  // shouji.cpp:47 (before the e >= m short-circuit)
+    if (!magnet && (width < 3 || width > 8)) {
         set_err(err, PF_ERR_INVALID_PARAMETERS, "window width must be in [3, 8]");
         return PF_ERR_INVALID_PARAMETERS;
     }
     uint32_t acc = 0;
-    const int st = pf_shouji_filter_batch(ctx, reinterpret_cast<const uint8_t*>(text),
-                                          reinterpret_cast<const uint8_t*>(pattern), text_len, 1,
-                                          static_cast<uint32_t>(text_len), e, width, &acc, estimate,
-                                          bits, err);
+    const auto* t = reinterpret_cast<const uint8_t*>(text);
+    const auto* p = reinterpret_cast<const uint8_t*>(pattern);
+    const auto m = static_cast<uint32_t>(text_len);
+    const int st = magnet ? pf_magnet_filter_batch(ctx, t, p, text_len, 1, m, e, &acc, estimate,
+                                                   bits, err)
+                          : pf_shouji_filter_batch(ctx, t, p, text_len, 1, m, e, width, &acc,
+                                                   estimate, bits, err);
     if (st != PF_OK) return st;
     *accept = static_cast<int>(acc & 1u);
     return PF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pf_shouji_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, const char* text,
+                         size_t text_len, uint32_t e, uint32_t width, int* accept,
+                         uint32_t* estimate, uint64_t* bits, pf_error* err) {
+    return filter_one(ctx, false, pattern, pattern_len, text, text_len, e, width, accept, estimate,
+                      bits, err);
+}
+
+int pf_magnet_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, const char* text,
+                         size_t text_len, uint32_t e, int* accept, uint32_t* estimate,
+                         uint64_t* bits, pf_error* err) {
+    return filter_one(ctx, true, pattern, pattern_len, text, text_len, e, 4, accept, estimate,
+                      bits, err);
 }
 
 void* pf_host_alloc(size_t bytes) {

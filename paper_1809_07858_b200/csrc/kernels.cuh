@@ -74,6 +74,14 @@ cudaError_t launch_repitch(const uint8_t* src, size_t src_stride, uint8_t* dst, 
 // Exact Levenshtein distance per pair (Myers bit-vector); out[i] = d <= e ? d : -1.
 cudaError_t launch_edit_distance(const uint8_t* text, const uint8_t* pattern, size_t pitch,
                                  long long n, int m, int e, int32_t* out, cudaStream_t s);
+// MAGNET (magnet.cu): one thread per pair, validated ASCII records, 0 <= e < m,
+// m <= kMagnetMaxM. Writes the accept bitmap, optional u32 estimates and
+// optional tally bits [n][ceil(m/64)] u64.
+constexpr int kMagnetMaxM = 512;
+bool magnet_supported(int m);
+cudaError_t launch_magnet(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
+                          int m, int e, uint32_t* accept, uint32_t* estimates, uint64_t* bits,
+                          cudaStream_t s);
 // e >= m short-circuit outputs.
 cudaError_t launch_accept_all(long long n, int m, uint32_t* accept, uint32_t* estimates,
                               uint64_t* bits, cudaStream_t s);
