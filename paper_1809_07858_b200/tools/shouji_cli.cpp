@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <initializer_list>
 #include <iostream>
 #include <iterator>
 #include <map>
@@ -190,9 +191,26 @@ void emit_report(const std::string& text, const std::string& file) {
 
 bool bit(const std::vector<uint32_t>& bm, size_t i) { return (bm[i / 32] >> (i % 32)) & 1u; }
 
+// run_filter(algo, ...) over the whole dataset (evaluate.cpp:13-21): Shouji or MAGNET.
+int run_algo(pf_ctx* ctx, const std::string& algo, const uint8_t* text, const uint8_t* pattern,
+             size_t n, uint32_t m, uint32_t e, uint32_t width, uint32_t* acc, uint32_t* est,
+             pf_error* err) {
+    if (algo == "magnet")
+        return pf_magnet_filter_batch(ctx, text, pattern, m, n, m, e, acc, est, nullptr, err);
+    return pf_shouji_filter_batch(ctx, text, pattern, m, n, m, e, width, acc, est, nullptr, err);
+}
+
+void require_algo(const std::string& algo, std::initializer_list<const char*> allowed) {
+    std::string names;
+    for (const char* a : allowed) {
+        if (algo == a) return;
+        names += (names.empty() ? "" : ", ") + std::string(a);
+    }
+    throw usage_error("--algo " + algo + " is not one of: " + names);
+}
+
 int cmd_filter(const options& o) {
-    if (o.algo != "shouji" && o.algo != "oracle")
-        throw usage_error("--algo " + o.algo + " is not provided by this build (shouji, oracle)");
+    require_algo(o.algo, {"shouji", "magnet", "oracle"});
     ctx_holder ch;
     dataset_holder dh;
     const uint32_t e = resolve_input(o, ch, dh);
@@ -207,8 +225,8 @@ int cmd_filter(const options& o) {
                                             m, n, m, e, dist.data(), &err),
               err);
     } else {
-        check(pf_shouji_filter_batch(ch.get(), pf_dataset_text(dh.ds), pf_dataset_pattern(dh.ds), m, n,
-                                     m, e, o.width, acc.data(), est.data(), nullptr, &err),
+        check(run_algo(ch.get(), o.algo, pf_dataset_text(dh.ds), pf_dataset_pattern(dh.ds), n, m, e,
+                       o.width, acc.data(), est.data(), &err),
               err);
     }
     std::string out;
@@ -245,7 +263,7 @@ int cmd_filter(const options& o) {
 }
 
 int cmd_eval(const options& o) {
-    if (o.algo != "shouji") throw usage_error("--algo " + o.algo + " is not provided by this build");
+    require_algo(o.algo, {"shouji", "magnet"});
     ctx_holder ch;
     dataset_holder dh;
     const uint32_t e = resolve_input(o, ch, dh);
@@ -254,8 +272,8 @@ int cmd_eval(const options& o) {
     std::vector<uint32_t> acc((n + 31) / 32), est(n);
     std::vector<int32_t> dist(n);
     pf_error err{};
-    check(pf_shouji_filter_batch(ch.get(), pf_dataset_text(dh.ds), pf_dataset_pattern(dh.ds), m, n, m,
-                                 e, o.width, acc.data(), est.data(), nullptr, &err),
+    check(run_algo(ch.get(), o.algo, pf_dataset_text(dh.ds), pf_dataset_pattern(dh.ds), n, m, e,
+                   o.width, acc.data(), est.data(), &err),
           err);
     check(pf_banded_edit_distance_batch(ch.get(), pf_dataset_text(dh.ds), pf_dataset_pattern(dh.ds), m,
                                         n, m, e, dist.data(), &err),
@@ -315,7 +333,7 @@ int cmd_gen(const options& o) {
 // run_bench (bench.cpp:11-42) on the GPU path: 1 warm-up + repeats passes of
 // the batch call over pre-generated pairs, median reported.
 int cmd_bench(const options& o) {
-    if (o.algo != "shouji") throw usage_error("--algo " + o.algo + " is not provided by this build");
+    require_algo(o.algo, {"shouji", "magnet"});
     const auto lens = parse_list(o.len, "--len");
     const auto es = parse_list(o.e, "--e");
     const size_t count = o.count ? o.count : 10000;
@@ -336,9 +354,8 @@ int cmd_bench(const options& o) {
             std::vector<double> secs;
             for (unsigned r = 0; r <= o.repeats; ++r) {
                 const auto t0 = std::chrono::steady_clock::now();
-                check(pf_shouji_filter_batch(ch.get(), pf_dataset_text(dh.ds), pf_dataset_pattern(dh.ds),
-                                             lens[li], count, lens[li], es[ei], o.width, acc.data(),
-                                             nullptr, nullptr, &err),
+                check(run_algo(ch.get(), o.algo, pf_dataset_text(dh.ds), pf_dataset_pattern(dh.ds),
+                               count, lens[li], es[ei], o.width, acc.data(), nullptr, &err),
                       err);
                 const double s =
                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

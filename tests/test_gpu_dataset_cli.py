@@ -160,3 +160,39 @@ def test_cli_bench_runs(gpu):
     lines = out.decode().splitlines()
     assert lines[0].startswith("algo,m,e,count,repeats,median_seconds")
     assert len([l for l in lines if l.startswith("shouji,")]) == 4 + 2
+
+
+def test_cli_magnet_filter_and_eval(gpu, oracle, reference):
+    """--algo magnet routes filter/eval/bench through pf_magnet_filter_batch (run_filter's
+    other branch, evaluate.cpp:13-21)."""
+    rc, out, err = run("filter", "--seed", "5", "--count", "6000", "--len", "150", "--e", "7",
+                       "--algo", "magnet", "--verbose")
+    assert rc == 0, err
+    t, p = oracle.generate_pairs(5, 6000, 150, 0, 14)
+    acc, est = reference.magnet_batch(t, p, 7)
+    bits = np.unpackbits(acc.view(np.uint8), bitorder="little")[:6000]
+    assert out == b"".join(b"%d\t%d\n" % (bits[i], est[i]) for i in range(6000))
+    assert json.loads(err)["algo"] == "magnet"
+    rc, out, err = run("eval", "--seed", "1105", "--count", "20000", "--len", "100", "--edits",
+                       "0..5", "--e", "5", "--algo", "magnet")
+    assert rc == 0, err
+    rep = json.loads(err)
+    t, p = oracle.generate_pairs(1105, 20000, 100, 0, 5)
+    acc, _ = reference.magnet_batch(t, p, 5)
+    packed = reference.pack(t, p)
+    try:
+        d = packed.banded(5)
+    finally:
+        packed.free()
+    a = np.unpackbits(acc.view(np.uint8), bitorder="little")[:20000].astype(bool)
+    within = d >= 0
+    assert rep["filter_accepted"] == int(a.sum())
+    assert rep["falsely_rejected"] == int((within & ~a).sum())
+    assert rep["falsely_accepted"] == int((~within & a).sum())
+    rc, out, err = run("bench", "--len", "100", "--e", "5", "--count", "20000", "--repeats", "1",
+                       "--algo", "magnet")
+    assert rc == 0, err
+    assert out.decode().splitlines()[1].startswith("magnet,100,5,20000,1,")
+    rc, _, err = run("filter", "--seed", "5", "--count", "10", "--len", "10", "--e", "1",
+                     "--algo", "nope")
+    assert rc == 1 and b"--algo" in err  # usage errors exit 1 (cli.cpp:357-359)
