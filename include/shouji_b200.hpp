@@ -6,6 +6,7 @@
 //   bitvector            proj/include/prefilter/bitvector.hpp:16-129 (read side)
 //   filter_decision      proj/include/prefilter/filter_decision.hpp:12-16
 //   shouji_filter        proj/include/prefilter/shouji.hpp:57-59
+//   magnet_filter        proj/include/prefilter/magnet.hpp:55-57
 //   error hierarchy      proj/include/prefilter/errors.hpp:11-84
 // plus a batch call (the fast path) that replaces run_filter + parallel_for_pairs
 // (proj/src/evaluate.cpp:13-48). Every decision is computed on the GPU by
@@ -243,6 +244,46 @@ inline batch_result shouji_filter_batch(const std::uint8_t* text, const std::uin
     if (estimates) r.estimates.assign(n, 0);
     pf_error err{};
     const int st = pf_shouji_filter_batch(ctx.get(), text, pattern, stride, n, m, e, width,
+                                          r.accept_bitmap.data(),
+                                          estimates ? r.estimates.data() : nullptr, nullptr, &err);
+    throw_status(st, err);
+    return r;
+}
+
+// ---- MAGNET (proj/src/magnet.cpp) -------------------------------------------------
+// magnet_filter(pattern = read, text = reference segment, e) — magnet.hpp:55-57.
+inline filter_decision magnet_filter(const packed_sequence& pattern, const packed_sequence& text,
+                                     std::uint32_t e, context& ctx = context::default_context()) {
+    pf_error err{};
+    int accept = 0;
+    std::uint32_t est = 0;
+    std::vector<std::uint64_t> words((text.size() + 63) / 64 + 1, 0);
+    const int st = pf_magnet_filter_one(ctx.get(), pattern.data(), pattern.size(), text.data(),
+                                        text.size(), e, &accept, &est, words.data(), &err);
+    throw_status(st, err);
+    return {accept != 0, est, bitvector::from_words(std::move(words), text.size())};
+}
+
+// filter_algo / run_filter (evaluate.hpp:11-19, evaluate.cpp:13-21).
+enum class filter_algo { shouji, magnet };
+inline filter_decision run_filter(filter_algo algo, const packed_sequence& pattern,
+                                  const packed_sequence& text, std::uint32_t e,
+                                  unsigned width = default_window_width,
+                                  context& ctx = context::default_context()) {
+    return algo == filter_algo::magnet ? magnet_filter(pattern, text, e, ctx)
+                                       : shouji_filter(pattern, text, e, width, ctx);
+}
+
+// MAGNET over n pairs of ASCII records (layout as shouji_filter_batch).
+inline batch_result magnet_filter_batch(const std::uint8_t* text, const std::uint8_t* pattern,
+                                        std::size_t stride, std::size_t n, std::uint32_t m,
+                                        std::uint32_t e, bool estimates = false,
+                                        context& ctx = context::default_context()) {
+    batch_result r;
+    r.accept_bitmap.assign((n + 31) / 32, 0);
+    if (estimates) r.estimates.assign(n, 0);
+    pf_error err{};
+    const int st = pf_magnet_filter_batch(ctx.get(), text, pattern, stride, n, m, e,
                                           r.accept_bitmap.data(),
                                           estimates ? r.estimates.data() : nullptr, nullptr, &err);
     throw_status(st, err);

@@ -153,6 +153,35 @@ int main() {
                                             m, 5),
                         illegal_character_error);
     }
+    {  // MAGNET through the same mirror (proj/tests/test_magnet.cpp:79-91,150-170)
+        const auto d = magnet_filter(seq("GGTGAGAGTTGT"), seq("GGTGCAGAGCTC"), 3);
+        CHECK(d.accept && d.edit_estimate == 3 && d.bits.count_zeros() == 9);
+        CHECK(d.bits.to_string() == "000010000101");
+        const auto big = magnet_filter(seq("ACGT"), seq("TGCA"), 7);
+        CHECK(big.accept && big.edit_estimate == 0);
+        CHECK_THROWS_AS(magnet_filter(seq("ACGT"), seq("ACG"), 1), length_mismatch_error);
+        const auto via = run_filter(filter_algo::magnet, seq("GGTGAGAGTTGT"), seq("GGTGCAGAGCTC"), 3);
+        CHECK(via.edit_estimate == 3);
+        std::mt19937_64 rng(59);
+        const std::size_t n = 2048, m = 150;
+        std::string t(n * m, 'A'), p(n * m, 'A');
+        for (std::size_t i = 0; i < n; ++i) {
+            const auto a = random_dna(rng, m);
+            auto b = a;
+            for (int k = 0; k < 8; ++k) b[rng() % m] = "ACGT"[rng() % 4];
+            t.replace(i * m, m, a);
+            p.replace(i * m, m, b);
+        }
+        const auto r = magnet_filter_batch(reinterpret_cast<const std::uint8_t*>(t.data()),
+                                           reinterpret_cast<const std::uint8_t*>(p.data()), m, n,
+                                           m, 7, true);
+        for (std::size_t i = 0; i < n; i += 61) {
+            const auto one = magnet_filter(seq(p.substr(i * m, m)), seq(t.substr(i * m, m)), 7);
+            CHECK(one.accept == r.accepted(i));
+            CHECK(one.edit_estimate == r.estimates[i]);
+            CHECK(one.edit_estimate == one.bits.count_ones());
+        }
+    }
     std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "PASS", failures);
     return failures;
 }
