@@ -169,6 +169,29 @@ int pf_shouji_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, c
                          size_t text_len, uint32_t e, uint32_t width, int* accept,
                          uint32_t* estimate, uint64_t* bits, pf_error* err);
 
+/* ---- Packed-planes variant --------------------------------
+ * Pairs the caller already packed with packed_sequence::from_string
+ * (proj/src/packed_sequence.cpp:7-34), passed in that class's own storage:
+ * per pair and sequence pf_packed_words(m) = 3 * ceil(m/64) uint64 words,
+ * low_plane then high_plane then n_plane (packed_sequence.hpp:50-53), each
+ * LSB-first (bit j of word w = base 64w+j; bits >= m ignored):
+ *   text_planes[i * pf_packed_words(m) + k * ceil(m/64) + w]
+ * This is the input run_bench times (pairs pre-packed, bench.cpp:24-25). No
+ * validation is needed (packing validated); the width check and the e >= m
+ * short-circuit follow shouji.cpp:47-49. Host arrays may be pinned (DMA'd in
+ * place) or pageable (staged through pinned buffers in 1Mi-pair chunks). */
+size_t pf_packed_words(uint32_t m);
+int pf_shouji_filter_packed_batch(pf_ctx* ctx, const uint64_t* text_planes,
+                                  const uint64_t* pattern_planes, size_t n, uint32_t m, uint32_t e,
+                                  uint32_t width, uint32_t* accept_bitmap, uint32_t* estimates,
+                                  uint64_t* bits, pf_error* err);
+/* Same on device-resident plane arrays (8-byte aligned), stream-ordered. */
+int pf_shouji_filter_packed_device(pf_ctx* ctx, const uint64_t* d_text_planes,
+                                   const uint64_t* d_pattern_planes, size_t n, uint32_t m,
+                                   uint32_t e, uint32_t width, uint32_t* d_accept_bitmap,
+                                   uint32_t* d_estimates, uint64_t* d_bits, void* stream,
+                                   pf_error* err);
+
 /* ---- MAGNET (proj/src/magnet.cpp) --------------------------
  * magnet_filter(pattern, text, e) (magnet.cpp:77-87) over a batch: e+1
  * extract-and-encapsulate steps over the 2e+1 diagonals; estimate =

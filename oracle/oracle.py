@@ -206,6 +206,7 @@ class Reference:
                                        C.POINTER(C.c_int), C.POINTER(C.c_uint32), C.c_char_p,
                                        C.c_int64, C.c_void_p, C.c_size_t,
                                        C.POINTER(C.c_size_t), C.c_char_p]
+        lib.ref_export_planes.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         lib.ref_longest_zero_run.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t, C.c_size_t,
                                              C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
         self.lib = lib
@@ -318,6 +319,14 @@ class _Packed:
         if st:
             raise OracleError(st)
         return acc, est
+
+    def planes(self):
+        """The reference's own packed_sequence planes: (text, pattern) u64[n, 3, ceil(m/64)]."""
+        w = (self.m + 63) // 64
+        t = np.zeros((self.n, 3, w), np.uint64)
+        p = np.zeros((self.n, 3, w), np.uint64)
+        self.ref.lib.ref_export_planes(self.h, _ptr(t), _ptr(p))
+        return t, p
 
     def banded(self, e, threads=None):
         threads = threads or self.ref.hardware_concurrency() or 1

@@ -309,6 +309,25 @@ int ref_magnet_one(const char* pattern, std::size_t pattern_len, const char* tex
     }
 }
 
+// The packed_sequence planes of a packed batch (packed_sequence.hpp:44-53):
+// out[i][k][w], k = 0 low_plane, 1 high_plane, 2 n_plane, ceil(m/64) words.
+void ref_export_planes(void* handle, std::uint64_t* text_out, std::uint64_t* pattern_out) {
+    auto* h = static_cast<dataset_handle*>(handle);
+    for (std::size_t i = 0; i < h->text.size(); ++i) {
+        for (int f = 0; f < 2; ++f) {
+            const auto& ps = f == 0 ? h->text[i] : h->pattern[i];
+            std::uint64_t* out = (f == 0 ? text_out : pattern_out);
+            const std::size_t w = ps.low_plane().size();
+            std::uint64_t* dst = out + i * 3 * w;
+            for (std::size_t k = 0; k < w; ++k) {
+                dst[k] = ps.low_plane()[k];
+                dst[w + k] = ps.high_plane()[k];
+                dst[2 * w + k] = ps.n_plane()[k];
+            }
+        }
+    }
+}
+
 // longest_zero_run (proj/src/magnet.cpp:9-22) on a '0'/'1' string.
 void ref_longest_zero_run(const char* bits, std::size_t nbits, std::size_t lo, std::size_t hi,
                           std::size_t* start, std::size_t* len) {

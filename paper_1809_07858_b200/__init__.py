@@ -35,6 +35,10 @@ from .api import (  # noqa: F401
     shouji_filter_device,
     shouji_filter_device_async,
     int_peak,
+    packed_words,
+    pack_planes,
+    shouji_filter_packed_batch,
+    shouji_filter_packed_device,
     magnet_filter,
     magnet_filter_batch,
     magnet_filter_device,

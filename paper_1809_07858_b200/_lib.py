@@ -36,7 +36,8 @@ EXPORTED = [
     "pf_dataset_source", "pf_dataset_write_tsv", "pf_dataset_free", "pf_banded_edit_distance_batch",
     "pf_nibble_pitch", "pf_host_pack_nibbles", "pf_shouji_filter_nibbles_device",
     "pf_transfer_bytes", "pf_magnet_filter_batch", "pf_magnet_filter_device",
-    "pf_magnet_filter_one",
+    "pf_magnet_filter_one", "pf_packed_words", "pf_shouji_filter_packed_batch",
+    "pf_shouji_filter_packed_device",
 ]
 
 
@@ -99,6 +100,11 @@ def _bind(lib):
                                                     C.POINTER(PfError)]),
         "pf_nibble_pitch": (_sz, [_u32]),
         "pf_transfer_bytes": (None, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+        "pf_packed_words": (_sz, [_u32]),
+        "pf_shouji_filter_packed_batch": (C.c_int, [_vp, _vp, _vp, _sz, _u32, _u32, _u32, _vp, _vp,
+                                                    _vp, C.POINTER(PfError)]),
+        "pf_shouji_filter_packed_device": (C.c_int, [_vp, _vp, _vp, _sz, _u32, _u32, _u32, _vp,
+                                                     _vp, _vp, _vp, C.POINTER(PfError)]),
         "pf_magnet_filter_batch": (C.c_int, [_vp, _vp, _vp, _sz, _sz, _u32, _u32, _vp, _vp, _vp,
                                              C.POINTER(PfError)]),
         "pf_magnet_filter_device": (C.c_int, [_vp, _vp, _vp, _sz, _sz, _u32, _u32, _vp, _vp, _vp,

@@ -360,6 +360,68 @@ def shouji_filter_batch(text, pattern, e: int, width: int = default_window_width
     return acc, est, bv
 
 
+def packed_words(m: int) -> int:
+    """u64 words per sequence per pair in the packed-planes layout (3 * ceil(m/64))."""
+    return int(L.lib.pf_packed_words(int(m)))
+
+
+def pack_planes(records, m: int | None = None) -> np.ndarray:
+    """ASCII records u8[n, stride] -> packed_sequence planes u64[n, 3, ceil(m/64)]
+    (low, high, N; codes A/C/G/T = 0..3, packed_sequence.cpp:16-30). Host-side
+    layout helper for callers and tests; it does not validate (use
+    packed_sequence.from_string or the batch entry points for that)."""
+    rec = _as_records(records)
+    n, stride = rec.shape
+    m = stride if m is None else int(m)
+    a = rec[:, :m]
+    code = np.zeros(a.shape, np.uint8)
+    code[a == ord("C")] = 1
+    code[a == ord("G")] = 2
+    code[a == ord("T")] = 3
+    isn = a == ord("N")
+    w = (m + 63) // 64
+    out = np.zeros((n, 3, w), np.uint64)
+    for k, plane in enumerate(((code & 1) == 1, (code & 2) == 2, isn)):
+        bits = np.zeros((n, w * 64), np.uint8)
+        bits[:, :m] = plane & ~isn if k < 2 else plane
+        out[:, k, :] = np.packbits(bits.reshape(n, w, 64), axis=2, bitorder="little").view(np.uint64)[:, :, 0]
+    return out
+
+
+def shouji_filter_packed_batch(text_planes, pattern_planes, m: int, e: int,
+                               width: int = default_window_width, estimates: bool = False,
+                               bits: bool = False, ctx: Context | None = None):
+    """Filter N pre-packed pairs (u64[n, 3, ceil(m/64)] each, see pack_planes)."""
+    ctx = ctx or default_context()
+    tp = np.ascontiguousarray(text_planes, np.uint64)
+    pp = np.ascontiguousarray(pattern_planes, np.uint64)
+    n = tp.shape[0]
+    if tp.shape != pp.shape or tp.size != n * packed_words(m):
+        raise length_mismatch_error("plane arrays must both be [n, 3, ceil(m/64)]")
+    acc = np.zeros((n + 31) // 32, np.uint32)
+    est = np.zeros(n, np.uint32) if estimates else None
+    bv = np.zeros((n, (m + 63) // 64), np.uint64) if bits else None
+    err = L.PfError()
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p) if a is not None else None  # noqa: E731
+    st = L.lib.pf_shouji_filter_packed_batch(ctx.handle, ptr(tp), ptr(pp), n, int(m), int(e),
+                                             int(width), ptr(acc), ptr(est), ptr(bv), C.byref(err))
+    _raise(st, err)
+    return acc, est, bv
+
+
+def shouji_filter_packed_device(d_text_planes: int, d_pattern_planes: int, n: int, m: int, e: int,
+                                d_accept: int, width: int = default_window_width,
+                                d_estimates: int | None = None, d_bits: int | None = None,
+                                stream: int | None = None, ctx: Context | None = None) -> None:
+    """Pre-packed planes already on the device (raw pointers)."""
+    ctx = ctx or default_context()
+    err = L.PfError()
+    st = L.lib.pf_shouji_filter_packed_device(ctx.handle, d_text_planes, d_pattern_planes, n, m,
+                                              int(e), int(width), d_accept, d_estimates, d_bits,
+                                              stream, C.byref(err))
+    _raise(st, err)
+
+
 def magnet_filter_batch(text, pattern, e: int, m: int | None = None, estimates: bool = False,
                         bits: bool = False, ctx: Context | None = None):
     """MAGNET over N pairs of host ASCII records (same layout and returns as

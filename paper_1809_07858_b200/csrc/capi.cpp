@@ -61,6 +61,12 @@ struct DeviceState {
     uint8_t* d_nib[2] = {nullptr, nullptr};
     size_t d_nib_bytes[2] = {0, 0};
     cudaEvent_t nib_ev[2] = {nullptr, nullptr};
+    // packed-planes input: device chunk buffers (text, pattern) and pinned staging
+    uint64_t* d_pk[2] = {nullptr, nullptr};
+    size_t d_pk_words[2] = {0, 0};
+    uint64_t* h_pk[2] = {nullptr, nullptr};
+    size_t h_pk_words = 0;
+    cudaEvent_t pk_ev[2] = {nullptr, nullptr};
 };
 
 }  // namespace
@@ -664,6 +670,9 @@ void pf_ctx_destroy(pf_ctx* ctx) {
             if (d.h_nib[b]) cudaFreeHost(d.h_nib[b]);
             cudaFree(d.d_nib[b]);
             if (d.nib_ev[b]) cudaEventDestroy(d.nib_ev[b]);
+            if (d.h_pk[b]) cudaFreeHost(d.h_pk[b]);
+            cudaFree(d.d_pk[b]);
+            if (d.pk_ev[b]) cudaEventDestroy(d.pk_ev[b]);
         }
         cudaFree(d.pipe.planes[0]);
         cudaFree(d.pipe.planes[1]);
@@ -686,6 +695,120 @@ int pf_ctx_device_count(const pf_ctx* ctx) { return ctx ? static_cast<int>(ctx->
 }  // extern "C"
 
 namespace {
+
+// Pre-packed pairs [p0, p1) (packed_sequence plane words, pf_packed_words(m)
+// u64 per sequence per pair) on one device: chunked H2D (pinned caller
+// buffers are DMA'd in place, pageable ones are copied into double-buffered
+// pinned staging by the host pool while the previous chunk is in flight),
+// re-slice + search per chunk, outputs gathered at the end.
+void run_packed_shard(DeviceState& d, const uint64_t* text, const uint64_t* pattern, size_t p0,
+                      size_t p1, uint32_t m, uint32_t e, uint32_t width, uint32_t* accept_bitmap,
+                      uint32_t* estimates, uint64_t* bits, ShardResult* res) {
+    pf_error* err = &res->err;
+    auto fail = [&](int st) { res->status = st; };
+    auto cu = [&](cudaError_t ce, const char* what) {
+        if (ce == cudaSuccess) return true;
+        set_err(err, ce == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA, what, ce);
+        fail(ce == cudaErrorMemoryAllocation ? PF_ERR_OUT_OF_MEMORY : PF_ERR_CUDA);
+        return false;
+    };
+    const size_t n = p1 - p0;
+    if (n == 0) return;
+    if (cudaSetDevice(d.device) != cudaSuccess) return fail(PF_ERR_NO_DEVICE);
+    const size_t pw = pf_packed_words(m);  // u64 words per sequence per pair
+    const size_t ngroups = (n + 31) / 32;
+    const size_t wpp = (m + 63) / 64;
+    if (!cu(grow(d.d_accept, d.accept_words, ngroups), "alloc accept")) return;
+    if (estimates && !cu(grow(d.d_est, d.est_n, n), "alloc estimates")) return;
+    if (bits && !cu(grow(d.d_bits, d.bits_words, n * wpp), "alloc bits")) return;
+    if (e >= m) {  // shouji.cpp:48-49
+        if (!cu(sb::launch_accept_all(static_cast<long long>(n), static_cast<int>(m), d.d_accept,
+                                      estimates ? d.d_est : nullptr, bits ? d.d_bits : nullptr,
+                                      d.stream),
+                "accept_all"))
+            return;
+    } else {
+        const bool pinned = is_pinned(text) && is_pinned(pattern);
+        const long long chunk = std::min<long long>((static_cast<long long>(n) + 255) / 256 * 256,
+                                                    1ll << 20);
+        const size_t cwords = static_cast<size_t>(chunk) * pw;
+        for (int b = 0; b < 2; ++b) {
+            if (!cu(grow(d.d_pk[b], d.d_pk_words[b], 2 * cwords), "alloc packed chunk")) return;
+            if (!d.pk_ev[b] &&
+                !cu(cudaEventCreateWithFlags(&d.pk_ev[b], cudaEventDisableTiming), "event"))
+                return;
+        }
+        if (!pinned && d.h_pk_words < 2 * cwords) {
+            for (int b = 0; b < 2; ++b) {
+                if (d.h_pk[b]) cudaFreeHost(d.h_pk[b]);
+                d.h_pk[b] = nullptr;
+            }
+            d.h_pk_words = 0;
+            for (int b = 0; b < 2; ++b)
+                if (!cu(cudaHostAlloc(&d.h_pk[b], 2 * cwords * 8, cudaHostAllocPortable),
+                        "alloc packed staging"))
+                    return;
+            d.h_pk_words = 2 * cwords;
+        }
+        if (!cu(grow(d.d_scratch, d.scratch_words, sb::planes_scratch_words(chunk, m)),
+                "alloc planes"))
+            return;
+        if (bits && !cu(grow(d.d_outplanes, d.outplanes_words,
+                             size_t(m) * static_cast<size_t>((chunk + 31) / 32)),
+                        "alloc tally planes"))
+            return;
+        const long long nchunks = (static_cast<long long>(n) + chunk - 1) / chunk;
+        for (long long i = 0; i < nchunks; ++i) {
+            const int b = static_cast<int>(i & 1);
+            const long long lo = i * chunk;
+            const long long cn = std::min<long long>(chunk, static_cast<long long>(n) - lo);
+            const uint64_t* st = text + (p0 + lo) * pw;
+            const uint64_t* sp = pattern + (p0 + lo) * pw;
+            const size_t cb = static_cast<size_t>(cn) * pw * 8;
+            if (!pinned) {
+                // the DMA that last read this staging buffer (chunk i-2) must be done
+                if (i >= 2 && !cu(cudaEventSynchronize(d.pk_ev[b]), "staging wait")) return;
+                sb::host_copy_parallel(d.h_pk[b], st, cb);
+                sb::host_copy_parallel(d.h_pk[b] + cwords, sp, cb);
+                st = d.h_pk[b];
+                sp = d.h_pk[b] + cwords;
+            }
+            if (!cu(xfer(d.d_pk[b], st, cb, cudaMemcpyHostToDevice, d.stream), "H2D planes")) return;
+            if (!cu(xfer(d.d_pk[b] + cwords, sp, cb, cudaMemcpyHostToDevice, d.stream),
+                    "H2D planes"))
+                return;
+            if (!cu(cudaEventRecord(d.pk_ev[b], d.stream), "staging record")) return;
+            sb::FilterArgs a{};
+            a.packed_text = d.d_pk[b];
+            a.packed_pattern = d.d_pk[b] + cwords;
+            a.n = cn;
+            a.m = static_cast<int>(m);
+            a.e = e;
+            a.width = width;
+            a.accept = d.d_accept + lo / 32;
+            a.estimates = estimates ? d.d_est + lo : nullptr;
+            a.outplanes = bits ? d.d_outplanes : nullptr;
+            a.planes = d.d_scratch;
+            a.planes_words = d.scratch_words;
+            if (!cu(sb::launch_filter(a, d.stream), "filter kernel")) return;
+            if (bits && !cu(sb::launch_bits_transpose(d.d_outplanes, cn, static_cast<int>(m),
+                                                      d.d_bits + static_cast<size_t>(lo) * wpp,
+                                                      d.stream),
+                            "bits"))
+                return;
+        }
+    }
+    if (!cu(xfer(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
+                 cudaMemcpyDeviceToHost, d.stream), "D2H accept"))
+        return;
+    if (estimates && !cu(xfer(estimates + p0, d.d_est, n * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, d.stream), "D2H estimates"))
+        return;
+    if (bits && !cu(xfer(bits + p0 * wpp, d.d_bits, n * wpp * sizeof(uint64_t),
+                         cudaMemcpyDeviceToHost, d.stream), "D2H bits"))
+        return;
+    cu(cudaStreamSynchronize(d.stream), "sync");
+}
 
 int run_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t stride, size_t n,
               uint32_t m, uint32_t e, uint32_t width, uint32_t* accept_bitmap, uint32_t* estimates,
@@ -814,6 +937,105 @@ int pf_magnet_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
     else
         PF_CUDA(sb::launch_magnet(d_text, d_pattern, pitch, a.n, a.m, static_cast<int>(e),
                                   d_accept_bitmap, d_estimates, d_bits, s));
+    return PF_OK;
+}
+
+size_t pf_packed_words(uint32_t m) { return 3 * ((static_cast<size_t>(m) + 63) / 64); }
+
+int pf_shouji_filter_packed_batch(pf_ctx* ctx, const uint64_t* text_planes,
+                                  const uint64_t* pattern_planes, size_t n, uint32_t m, uint32_t e,
+                                  uint32_t width, uint32_t* accept_bitmap, uint32_t* estimates,
+                                  uint64_t* bits, pf_error* err) {
+    if (err) std::memset(err, 0, sizeof(*err));
+    if (!ctx) return PF_ERR_NULL_ARGUMENT;
+    if (n == 0) return PF_OK;
+    if (!text_planes || !pattern_planes || !accept_bitmap) return PF_ERR_NULL_ARGUMENT;
+    if (m == 0) {
+        set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
+        return PF_ERR_EMPTY_SEQUENCE;
+    }
+    if (width < 3 || width > 8) {  // window_zero_table ctor (shouji.cpp:9-15), before e >= m
+        set_err(err, PF_ERR_INVALID_PARAMETERS, "window width must be in [3, 8]");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    if (m >= (1u << 24)) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS, "m >= 2^24");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    const size_t nd = ctx->devs.size();
+    const size_t groups = (n + 31) / 32;
+    std::vector<size_t> bounds(nd + 1);
+    for (size_t t = 0; t <= nd; ++t) bounds[t] = std::min(n, groups * t / nd * 32);
+    std::vector<ShardResult> res(nd);
+    if (nd == 1) {
+        run_packed_shard(ctx->devs[0], text_planes, pattern_planes, bounds[0], bounds[1], m, e,
+                         width, accept_bitmap, estimates, bits, &res[0]);
+    } else {
+        std::vector<std::thread> pool;
+        for (size_t t = 0; t < nd; ++t)
+            pool.emplace_back(run_packed_shard, std::ref(ctx->devs[t]), text_planes,
+                              pattern_planes, bounds[t], bounds[t + 1], m, e, width,
+                              accept_bitmap, estimates, bits, &res[t]);
+        for (auto& th : pool) th.join();
+    }
+    for (size_t t = 0; t < nd; ++t) {
+        if (res[t].status != PF_OK) {
+            if (err) *err = res[t].err;
+            if (err) err->status = res[t].status;
+            return res[t].status;
+        }
+    }
+    return PF_OK;
+}
+
+int pf_shouji_filter_packed_device(pf_ctx* ctx, const uint64_t* d_text_planes,
+                                   const uint64_t* d_pattern_planes, size_t n, uint32_t m,
+                                   uint32_t e, uint32_t width, uint32_t* d_accept_bitmap,
+                                   uint32_t* d_estimates, uint64_t* d_bits, void* stream,
+                                   pf_error* err) {
+    if (err) std::memset(err, 0, sizeof(*err));
+    if (!ctx) return PF_ERR_NULL_ARGUMENT;
+    if (n == 0) return PF_OK;
+    if (!d_text_planes || !d_pattern_planes || !d_accept_bitmap) return PF_ERR_NULL_ARGUMENT;
+    if (m == 0) {
+        set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
+        return PF_ERR_EMPTY_SEQUENCE;
+    }
+    if (width < 3 || width > 8 || m >= (1u << 24) ||
+        (reinterpret_cast<uintptr_t>(d_text_planes) | reinterpret_cast<uintptr_t>(d_pattern_planes)) %
+                8 != 0) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS,
+                "window width must be in [3, 8]; plane arrays must be 8-byte aligned");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceState& d = ctx->devs[0];
+    PF_CUDA(cudaSetDevice(d.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (e >= m) {
+        PF_CUDA(sb::launch_accept_all(static_cast<long long>(n), static_cast<int>(m),
+                                      d_accept_bitmap, d_estimates, d_bits, s));
+        return PF_OK;
+    }
+    const size_t ngroups = (n + 31) / 32;
+    PF_CUDA(grow(d.d_scratch, d.scratch_words,
+                 sb::planes_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
+    if (d_bits) PF_CUDA(grow(d.d_outplanes, d.outplanes_words, size_t(m) * ngroups));
+    sb::FilterArgs a{};
+    a.packed_text = d_text_planes;
+    a.packed_pattern = d_pattern_planes;
+    a.n = static_cast<long long>(n);
+    a.m = static_cast<int>(m);
+    a.e = e;
+    a.width = width;
+    a.accept = d_accept_bitmap;
+    a.estimates = d_estimates;
+    a.outplanes = d_bits ? d.d_outplanes : nullptr;
+    a.planes = d.d_scratch;
+    a.planes_words = d.scratch_words;
+    PF_CUDA(sb::launch_filter(a, s));
+    if (d_bits) PF_CUDA(sb::launch_bits_transpose(d.d_outplanes, a.n, a.m, d_bits, s));
     return PF_OK;
 }
 

@@ -252,4 +252,20 @@ void host_pack_nibbles_parallel(const uint8_t* text, const uint8_t* pattern, siz
         if (b.any) bad->offer(b.pair, b.field, b.pos, b.byte);
 }
 
+void host_copy_parallel(void* dst, const void* src, size_t bytes) {
+    const size_t tasks = std::max<size_t>(
+        1, std::min<size_t>((bytes + (1u << 20) - 1) >> 20, 4ull * host_pack_threads()));
+    auto body = [&](size_t t) {
+        const size_t lo = bytes * t / tasks / 64 * 64;
+        const size_t hi = t + 1 == tasks ? bytes : bytes * (t + 1) / tasks / 64 * 64;
+        if (hi > lo)
+            std::memcpy(static_cast<uint8_t*>(dst) + lo, static_cast<const uint8_t*>(src) + lo,
+                        hi - lo);
+    };
+    if (tasks == 1)
+        body(0);
+    else
+        pool().run(tasks, body);
+}
+
 }  // namespace sb

@@ -38,6 +38,9 @@ void host_pack_nibbles_parallel(const uint8_t* text, const uint8_t* pattern, siz
                                 HostBad* bad, unsigned threads = 0, bool allow_simd = true);
 unsigned host_pack_threads();
 
+// memcpy on the same worker pool (pageable -> pinned staging copies).
+void host_copy_parallel(void* dst, const void* src, size_t bytes);
+
 // True when the AVX-512 (BW/VBMI) path is used on this host.
 bool host_pack_uses_simd();
 

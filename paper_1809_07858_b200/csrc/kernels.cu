@@ -282,19 +282,20 @@ cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
     if (a.n <= 0) return cudaSuccess;
     if (a.planes == nullptr || a.planes_words < plane_words(a.n, a.m)) return cudaErrorInvalidValue;
     const bool tile_ok = tile_smem(a.pitch, tile_groups(a.pitch)) <= 110 * 1024 && a.pitch % 4 == 0;
-    if (!a.nibbles && use_fused(a.width, a.e, a.m) && tile_ok && a.outplanes == nullptr &&
-        fused_enabled())
+    if (!a.nibbles && !a.packed_text && use_fused(a.width, a.e, a.m) && tile_ok &&
+        a.outplanes == nullptr && fused_enabled())
         return kFusedTable[a.e](a, s);
     cudaError_t st =
-        a.nibbles ? launch_pack_nibbles(a.text, a.pattern, a.n, a.m, a.planes, s)
-                  : launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, a.planes, a.err_flag, s);
+        a.packed_text ? launch_pack_planes(a.packed_text, a.packed_pattern, a.n, a.m, a.planes, s)
+        : a.nibbles   ? launch_pack_nibbles(a.text, a.pattern, a.n, a.m, a.planes, s)
+                      : launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, a.planes, a.err_flag, s);
     if (st != cudaSuccess) return st;
     if (use_fused(a.width, a.e, a.m)) return kSearchTable[a.e](a, s);
     return a.m <= 255 ? launch_generic<8>(a, s) : launch_generic<24>(a, s);
 }
 
 bool pipeline_applies(const FilterArgs& a, long long chunk) {
-    return chunk > 0 && a.n > chunk && a.outplanes == nullptr && !a.nibbles &&
+    return chunk > 0 && a.n > chunk && a.outplanes == nullptr && !a.nibbles && !a.packed_text &&
            use_fused(a.width, a.e, a.m);
 }
 

@@ -27,6 +27,8 @@ struct FilterArgs {
     uint32_t* planes;      // device scratch for the pair-sliced planes (pack.cuh)
     size_t planes_words;   // available words in planes
     bool nibbles;          // text/pattern are host-packed nibble records (pitch unused)
+    const uint64_t* packed_text;     // non-null: pre-packed planes input (pack_planes.cu);
+    const uint64_t* packed_pattern;  //   text/pattern/pitch unused
 };
 
 // Scratch words the filter needs for n pairs of length m.
@@ -40,6 +42,9 @@ cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitc
 bool nibble_pack_fits(int m);
 cudaError_t launch_pack_nibbles(const uint8_t* text, const uint8_t* pattern, long long n, int m,
                                 uint32_t* planes, cudaStream_t s);
+// Stage 1 from packed_sequence planes ([n][3][ceil(m/64)] u64 per sequence).
+cudaError_t launch_pack_planes(const uint64_t* text, const uint64_t* pattern, long long n, int m,
+                               uint32_t* planes, cudaStream_t s);
 // Launch the filter (pack + width-4 search, or pack + generic). Returns a cudaError_t.
 cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s);
 // Resources for the chunked, two-stream pipeline: pack of chunk i+1 (memory

@@ -122,3 +122,23 @@ def test_host_batch_first_illegal_byte_across_chunks(gpu):
     assert (ei.value.pair, ei.value.field, ei.value.position()) == (1_050_000, 1, 5)
     p[1_050_000, 5] = ord("A")
     gpu.shouji_filter_batch(t, p, 5)  # and the context still works
+
+
+def test_host_pack_with_device_shards(gpu, oracle):
+    """A context over several devices runs one host-pack stream per shard (here the
+    same device listed three times); results and first-error order are unchanged."""
+    rng = np.random.default_rng(21)
+    n = 600_001
+    t, p = mutated(rng, n, 100, alphabet=ACGT)
+    a_ref, e_ref, _ = oracle.shouji_batch(t, p, 5)
+    ctx = gpu.Context([0, 0, 0])
+    try:
+        a, e, _ = gpu.shouji_filter_batch(t, p, 5, estimates=True, ctx=ctx)
+        assert (a == a_ref).all() and (e == e_ref).all()
+        p[450_000, 1] = ord("#")  # third shard
+        t[250_000, 2] = ord("@")  # second shard: reported
+        with pytest.raises(gpu.illegal_character_error) as ei:
+            gpu.shouji_filter_batch(t, p, 5, ctx=ctx)
+        assert (ei.value.pair, ei.value.field, ei.value.position()) == (250_000, 0, 2)
+    finally:
+        ctx.close()
