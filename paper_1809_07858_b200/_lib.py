@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libshouji_b200.so")
+# PF_LIB_PATH: load another build of the same ABI (A/B experiments)
+LIB_PATH = os.environ.get("PF_LIB_PATH") or os.path.join(_HERE, "libshouji_b200.so")
 
 PF_OK = 0
 PF_ERR_EMPTY_SEQUENCE = 1
@@ -128,7 +129,7 @@ def load(path: str = LIB_PATH):
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is missing: build the sm_100a extension first "
-            "(python -m paper_1809_07858_b200.build or __graft_entry__.build()). "
+            "(python paper_1809_07858_b200/build.py or __graft_entry__.build()). "
             "There is no CPU fallback.")
     return _bind(C.CDLL(path))
 

@@ -81,6 +81,9 @@ struct SearchCfg {
     static constexpr bool CARRY = E <= 12;
     static constexpr int B = 4;  // windows per block
     static constexpr int NT = 128;
+    // 4 CTAs (16 warps) per SM where the carried D columns still fit 128
+    // registers without spilling (E <= 7); larger E keeps the compiler's choice.
+    static constexpr int MINB = E <= 7 ? 4 : 1;
 };
 
 // Column loads relative to a per-block base pointer: word (x*3 + k) * 8 of the
@@ -279,7 +282,7 @@ __device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes
 }
 
 template <int E>
-__global__ void __launch_bounds__(SearchCfg<E>::NT)
+__global__ void __launch_bounds__(SearchCfg<E>::NT, SearchCfg<E>::MINB)
 shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
                  uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
                  uint32_t* __restrict__ outplanes) {
