@@ -185,3 +185,18 @@ def test_oracle_generator_vs_reference(oracle, reference):
         t1, p1 = oracle.generate_pairs(seed, 5000, m, lo, hi)
         t2, p2 = reference.generate_pairs(seed, 5000, m, lo, hi)
         assert (t1 == t2).all() and (p1 == p2).all()
+
+
+def test_estimate_can_exceed_hamming(oracle, reference):
+    """The reference's comment "the estimate never exceeds the Hamming distance"
+    (proj/tests/test_shouji.cpp:163-166) is not a theorem: this substitution-only
+    pair (found in a 30M-pair config-1 run) has Hamming distance 2 and the
+    reference library's estimate at E=5 is 3. Parity follows the implementation,
+    so the oracle must agree with the library here, not with the comment."""
+    t = ("AATTGCCAATATCGATAGTTTCAGCTGAGGATCCATCTCGGCGCTTAATGGGATGAGGCCGAATCCAGGACGACGTATCGG"
+         "TCGGCGAGCAAGTTTACTG")
+    p = ("AATTGCCAATATCGATAGTTTCAGCTGAGGATCCATCTCGGCGCTTAATGGGATGAGGCCGAATCCAGGACGACGTATCGG"
+         "TCGGCGAGCACGGTTACTG")
+    assert sum(a != b for a, b in zip(t, p)) == 2
+    assert reference.shouji_one(p, t, 5)[1] == 3
+    assert oracle.shouji_one(p, t, 5) == reference.shouji_one(p, t, 5)
