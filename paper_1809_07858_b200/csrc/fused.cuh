@@ -197,6 +197,53 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
     }
 }
 
+// The commit chain over one block's windows (column order) and the tally
+// counter update: fsm_step4 per window, then the block's 4 tally bits are
+// added to the bit-sliced estimate counter.
+template <int B, int NC>
+__device__ __forceinline__ void commit_block(const Cand4 (&best)[B], uint32_t (&S)[3], int j0,
+                                             int m, long long g, long long ngroups,
+                                             uint32_t* __restrict__ outplanes,
+                                             uint32_t (&cnt)[NC]) {
+    static_assert(B == 4, "the tally adder below is written for 4 windows per block");
+    uint32_t outs[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        const int j = j0 + b;
+        outs[b] = 0u;
+        if (j >= 0 && j < m) {
+            outs[b] = fsm_step4(best[b], S);
+            if (outplanes) outplanes[static_cast<long long>(j) * ngroups + g] = outs[b];
+        }
+    }
+    uint32_t v[3];
+    const uint32_t s1 = outs[0] ^ outs[1] ^ outs[2];
+    const uint32_t c1 = (outs[0] & outs[1]) | (outs[0] & outs[2]) | (outs[1] & outs[2]);
+    v[0] = s1 ^ outs[3];
+    v[1] = c1 ^ (s1 & outs[3]);
+    v[2] = c1 & s1 & outs[3];
+    bs_add(cnt, v);
+}
+
+// accept = ones <= e (shouji.cpp:56-57); bits of pairs past n are 0.
+template <int E, int NC>
+__device__ __forceinline__ void finish_group(const uint32_t (&cnt)[NC], long long row0, long long n,
+                                             long long g, uint32_t* __restrict__ accept,
+                                             uint32_t* __restrict__ estimates) {
+    const long long valid = n - row0;
+    const uint32_t vmask = valid >= 32 ? ~0u : ((1u << valid) - 1u);
+    accept[g] = bs_le_const(cnt, static_cast<uint32_t>(E)) & vmask;
+    if (estimates) {
+#pragma unroll 1
+        for (int b = 0; b < 32 && b < valid; ++b) {
+            uint32_t est = 0;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) est |= ((cnt[i] >> b) & 1u) << i;
+            estimates[row0 + b] = est;
+        }
+    }
+}
+
 // The whole Shouji sweep for group g (32 pairs) from its planes.
 template <int E, bool NCLOAD>
 __device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes, long long g,
@@ -244,42 +291,183 @@ __device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes
             search_block<E, false, NCLOAD>(tbase, tcol0, pbase, pcol0, m, Dc, best);
         else
             search_block<E, true, NCLOAD>(tbase, tcol0, pbase, pcol0, m, Dc, best);
-        // commit chain over the block's windows, in column order
-        uint32_t outs[B];
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-            const int j = j0 + b;
-            outs[b] = 0u;
-            if (j >= 0 && j < m) {
-                outs[b] = fsm_step4(best[b], S);
-                if (outplanes) outplanes[static_cast<long long>(j) * ngroups + g] = outs[b];
-            }
-        }
-        uint32_t v[3];
-        {
-            const uint32_t s1 = outs[0] ^ outs[1] ^ outs[2];
-            const uint32_t c1 = (outs[0] & outs[1]) | (outs[0] & outs[2]) | (outs[1] & outs[2]);
-            v[0] = s1 ^ outs[3];
-            v[1] = c1 ^ (s1 & outs[3]);
-            v[2] = c1 & s1 & outs[3];
-        }
-        bs_add(cnt, v);
+        commit_block(best, S, j0, m, g, ngroups, outplanes, cnt);
     }
+    finish_group<E>(cnt, row0, n, g, accept, estimates);
+}
 
-    // accept = ones <= e (shouji.cpp:56-57); bits of pairs past n are 0.
-    const long long valid = n - row0;
-    const uint32_t vmask = valid >= 32 ? ~0u : ((1u << valid) - 1u);
-    accept[g] = bs_le_const(cnt, static_cast<uint32_t>(E)) & vmask;
-    if (estimates) {
-#pragma unroll 1
-        for (int b = 0; b < 32 && b < valid; ++b) {
-            uint32_t est = 0;
-#pragma unroll
-            for (int i = 0; i < NC; ++i) est |= ((cnt[i] >> b) & 1u) << i;
-            estimates[row0 + b] = est;
-        }
+// ---- prefetching form (CARRY, used for 7 <= E <= 12) ---------------------------
+// The same sweep, but the planes a block needs arrive one block ahead with
+// cp.async into a per-thread shared-memory region: a double-buffered text
+// slot (4 columns x 3 planes) and a pattern ring of R = 2E+8 columns (block
+// blk reads pattern columns [4blk-E, 4blk+4+E) while the 4 columns of block
+// blk+1 stream in). Each pattern column is fetched once (the direct form
+// reloads it (4+2E)/4 times from L1/L2) and the search reads shared memory
+// (~30-cycle latency) instead of waiting on global loads. Columns outside
+// [0, m) are written as N planes directly, so the search needs no bounds
+// checks. Per-thread regions have an odd word stride: the 32 lanes of a warp
+// reading the same offset hit 32 banks.
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
+template <int E>
+struct PfCfg {
+    static constexpr int R = 2 * E + 8;            // pattern ring columns
+    static constexpr int TEXT = 0;                 // [2][4][3] words
+    static constexpr int RING = 24;                // [R][3] words
+    static constexpr int WORDS = (24 + 3 * R) | 1;  // per-thread stride (odd)
+};
+
+// Column `col` of sequence planes `base` (the group's plane words, pack.cuh
+// layout) into dst[0..2]: cp.async in range, N planes outside.
+__device__ __forceinline__ void fetch_col(uint32_t* dst, const uint32_t* __restrict__ base, int col,
+                                          int m) {
+    constexpr int COLW = 3 * kPackGroups;
+    if (static_cast<unsigned>(col) < static_cast<unsigned>(m)) {
+        const uint32_t* src = base + static_cast<long long>(col) * COLW;
+        cp_async4(dst + 0, src);
+        cp_async4(dst + 1, src + kPackGroups);
+        cp_async4(dst + 2, src + 2 * kPackGroups);
+    } else {
+        dst[0] = 0u;
+        dst[1] = 0u;
+        dst[2] = ~0u;
     }
 }
+
+template <int E>
+__device__ __forceinline__ void search_group_pf(const uint32_t* __restrict__ planes, long long g,
+                                                long long n, int m, uint32_t* __restrict__ accept,
+                                                uint32_t* __restrict__ estimates,
+                                                uint32_t* __restrict__ outplanes,
+                                                uint32_t* __restrict__ region) {
+    using P = PfCfg<E>;
+    constexpr int B = 4;
+    constexpr int R = P::R;
+    constexpr int NC = 8;
+    const long long row0 = g * 32;
+    const long long ngroups = (n + 31) / 32;
+    const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
+    const int mc = plane_cols(m);
+    const bool live = row0 < n;
+    // dead threads still walk the blocks (uniform cp.async groups), on group 0's planes
+    const long long gg = live ? g : 0;
+    const uint32_t* const tb = planes + plane_index(0, gg, 0, 0, nblocks, mc);
+    const uint32_t* const pb = planes + plane_index(1, gg, 0, 0, nblocks, mc);
+    uint32_t* const text = region + P::TEXT;
+    uint32_t* const ring = region + P::RING;
+    auto ring_slot = [&](int col) { return ring + ((col + E) % R) * 3; };
+
+    uint32_t Dc[2 * E + 1][3];
+#pragma unroll
+    for (int di = 0; di <= 2 * E; ++di) Dc[di][0] = Dc[di][1] = Dc[di][2] = ~0u;
+    uint32_t S[3] = {~0u, ~0u, ~0u};
+    uint32_t cnt[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) cnt[i] = 0u;
+
+    const int NB = (m + 3 + B - 1) / B;
+    // prologue: block 0 (text columns 0..3, pattern columns [-E, 4+E))
+#pragma unroll
+    for (int b = 0; b < B; ++b) fetch_col(text + b * 3, tb, b, m);
+#pragma unroll 1
+    for (int c = -E; c < B + E; ++c) fetch_col(ring_slot(c), pb, c, m);
+    cp_async_commit();
+#pragma unroll 1
+    for (int blk = 0; blk < NB; ++blk) {
+        const int tcol0 = B * blk;
+        if (blk + 1 < NB) {
+            uint32_t* tn = text + ((blk + 1) & 1) * 12;
+#pragma unroll
+            for (int b = 0; b < B; ++b) fetch_col(tn + b * 3, tb, tcol0 + B + b, m);
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const int c = tcol0 + B + E + b;
+                fetch_col(ring_slot(c), pb, c, m);
+            }
+        }
+        cp_async_commit();
+        cp_async_wait1();  // block blk's columns have landed
+        const uint32_t* tc = text + (blk & 1) * 12;
+        uint32_t T[B][3];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            T[b][0] = tc[b * 3 + 0];
+            T[b][1] = tc[b * 3 + 1];
+            T[b][2] = tc[b * 3 + 2];
+        }
+        // pattern column tcol0 - E + x lives in ring slot (tcol0 + x) % R
+        const int base = tcol0 % R;
+        const int split = R - base;  // x >= split wraps to the ring's start
+        const uint32_t* lo = ring + base * 3;
+        const uint32_t* hi = ring + (base - R) * 3;
+        auto pcol = [&](int x, uint32_t (&v)[3]) {
+            const uint32_t* q = (x < split ? lo : hi) + x * 3;
+            v[0] = q[0];
+            v[1] = q[1];
+            v[2] = q[2];
+        };
+        Cand4 best[B];
+        uint32_t P4[B][3];
+#pragma unroll
+        for (int di = 0; di <= 2 * E; ++di) {
+            if (di == 0) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) pcol(b, P4[b]);
+            } else {
+#pragma unroll
+                for (int b = 0; b < B - 1; ++b) {
+                    P4[b][0] = P4[b + 1][0];
+                    P4[b][1] = P4[b + 1][1];
+                    P4[b][2] = P4[b + 1][2];
+                }
+                pcol(B - 1 + di, P4[B - 1]);
+            }
+            uint32_t sv[B + 3];
+            sv[0] = Dc[di][0];
+            sv[1] = Dc[di][1];
+            sv[2] = Dc[di][2];
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+                sv[3 + b] = (P4[b][0] ^ T[b][0]) | (P4[b][1] ^ T[b][1]) | P4[b][2] | T[b][2];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                Cand4 cd;
+                make_cand4(sv[b], sv[b + 1], sv[b + 2], sv[b + 3], cd);
+                if (di == 0)
+                    best[b] = cd;
+                else
+                    update_best4(cd, best[b]);
+            }
+            Dc[di][0] = sv[B];
+            Dc[di][1] = sv[B + 1];
+            Dc[di][2] = sv[B + 2];
+        }
+        commit_block(best, S, tcol0 - 3, m, g, ngroups, live ? outplanes : nullptr, cnt);
+    }
+    if (live) finish_group<E>(cnt, row0, n, g, accept, estimates);
+}
+
+template <int E>
+__global__ void __launch_bounds__(SearchCfg<E>::NT, SearchCfg<E>::MINB)
+shouji_search_w4_pf(const uint32_t* __restrict__ planes, long long n, int m,
+                    uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
+                    uint32_t* __restrict__ outplanes) {
+    extern __shared__ uint32_t pf_smem[];
+    const long long g = static_cast<long long>(blockIdx.x) * SearchCfg<E>::NT + threadIdx.x;
+    search_group_pf<E>(planes, g, n, m, accept, estimates, outplanes,
+                       pf_smem + threadIdx.x * PfCfg<E>::WORDS);
+}
+
+bool search_prefetch_enabled();
 
 template <int E>
 __global__ void __launch_bounds__(SearchCfg<E>::NT, SearchCfg<E>::MINB)
@@ -327,6 +515,26 @@ cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s) {
     using Cfg = SearchCfg<E>;
     const long long ngroups = (a.n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + Cfg::NT - 1) / Cfg::NT);
+    // measured on B200 (tools/exp_e_sweep.py, m=100): the prefetching form wins
+    // from E = 7 (+1%) to E = 12 (+7% at E = 10) and loses below (its per-block
+    // fetch bookkeeping outweighs the hidden latency when there are few diagonals)
+    if constexpr (Cfg::CARRY && E >= 7) {
+        if (search_prefetch_enabled()) {
+            const size_t smem = static_cast<size_t>(Cfg::NT) * PfCfg<E>::WORDS * 4;
+            static bool attr = false;
+            if (!attr) {
+                const cudaError_t st = cudaFuncSetAttribute(
+                    shouji_search_w4_pf<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    static_cast<int>(smem));
+                if (st != cudaSuccess) return st;
+                attr = true;
+            }
+            shouji_search_w4_pf<E><<<grid, Cfg::NT, smem, s>>>(a.planes, a.n, a.m, a.accept,
+                                                              a.estimates, a.outplanes);
+            count_launch();
+            return cudaGetLastError();
+        }
+    }
     shouji_search_w4<E><<<grid, Cfg::NT, 0, s>>>(a.planes, a.n, a.m, a.accept, a.estimates,
                                                   a.outplanes);
     count_launch();

@@ -241,6 +241,15 @@ static constexpr auto kFusedTable =
 
 // One-kernel pack+search (shouji_fused_w4) only when PF_FUSED=1: measured
 // slower than pack + search on B200 (profiles/r1_notes.md), kept for A/B runs.
+// Prefetching search (fused.cuh shouji_search_w4_pf): PF_SEARCH_PF=0 turns it off.
+bool search_prefetch_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("PF_SEARCH_PF");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 static bool fused_enabled() {
     static const bool v = [] {
         const char* e = std::getenv("PF_FUSED");
