@@ -89,7 +89,8 @@ def test_lengths(gpu, oracle, m):
     t, p = related(rng, n, m)
     half = n // 2
     p[half:] = ACGTN[rng.integers(0, 5, size=(n - half, m))]  # unrelated half
-    for e in sorted({0, 1, min(m - 1, 4), min(m - 1, 10), min(m - 1, 25), m - 1, m, m + 3}):
+    for e in sorted({0, 1, min(m - 1, 4), min(m - 1, 10), min(m - 1, 13), min(m - 1, 25),
+                     min(m - 1, 31), m - 1, m, m + 3}):
         check(gpu, oracle, t, p, e)
 
 
@@ -170,3 +171,13 @@ def test_errors(gpu):
     big = np.full((2, 600), ord("A"), np.uint8)
     a, est, _ = gpu.magnet_filter_batch(big, big, 600, estimates=True)
     assert int(a[0]) == 3 and (est == 0).all()
+
+
+def test_warp_and_thread_forms_agree(gpu, oracle):
+    """E in [13, 31] runs the warp-cooperative kernel; both forms against the oracle
+    around the switch-over and at the warp form's 2-diagonals-per-lane edge."""
+    rng = np.random.default_rng(77)
+    for m in (100, 250):
+        t, p = related(rng, 1200, m, rate=0.1, shifts=4)
+        for e in (12, 13, 15, 16, 31):
+            check(gpu, oracle, t, p, e)
