@@ -521,14 +521,9 @@ cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s) {
     if constexpr (Cfg::CARRY && E >= 7) {
         if (search_prefetch_enabled()) {
             const size_t smem = static_cast<size_t>(Cfg::NT) * PfCfg<E>::WORDS * 4;
-            static bool attr = false;
-            if (!attr) {
-                const cudaError_t st = cudaFuncSetAttribute(
-                    shouji_search_w4_pf<E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                    static_cast<int>(smem));
-                if (st != cudaSuccess) return st;
-                attr = true;
-            }
+            const cudaError_t st =
+                ensure_smem_attr<shouji_search_w4_pf<E>>(static_cast<int>(smem));
+            if (st != cudaSuccess) return st;
             shouji_search_w4_pf<E><<<grid, Cfg::NT, smem, s>>>(a.planes, a.n, a.m, a.accept,
                                                               a.estimates, a.outplanes);
             count_launch();
@@ -545,13 +540,8 @@ template <int E>
 cudaError_t launch_fused_e(const FilterArgs& a, cudaStream_t s) {
     const int groups = tile_groups(a.pitch);
     const size_t smem = tile_smem(a.pitch, groups);
-    static bool attr = false;  // per instantiation; idempotent
-    if (!attr) {
-        cudaError_t st = cudaFuncSetAttribute(shouji_fused_w4<E>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
-        if (st != cudaSuccess) return st;
-        attr = true;
-    }
+    const cudaError_t st = ensure_smem_attr<shouji_fused_w4<E>>(110 * 1024);
+    if (st != cudaSuccess) return st;
     const long long ngroups = (a.n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + kFusedNT - 1) / kFusedNT);
     shouji_fused_w4<E><<<grid, kFusedNT, smem, s>>>(a.text, a.pattern, a.pitch, a.n, a.m, groups,

@@ -2,11 +2,28 @@
 // kernels (kernels.cu). Not installed; not part of the public boundary.
 #pragma once
 #include <cstddef>
+#include <atomic>
 #include <cstdint>
 
 #include <cuda_runtime.h>
 
 namespace sb {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute belongs to the device's context, so a context spanning several
+// devices must set it on each (one bit per device ordinal).
+template <auto Kernel>
+cudaError_t ensure_smem_attr(int bytes) {
+    static std::atomic<unsigned long long> done{0};
+    int dev = 0;
+    cudaError_t st = cudaGetDevice(&dev);
+    if (st != cudaSuccess) return st;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    st = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (st == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return st;
+}
 
 // Largest E served by the fused, E-specialised width-4 kernel; larger E and
 // widths other than 4 run the two-kernel generic path.

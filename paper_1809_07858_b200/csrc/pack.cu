@@ -56,14 +56,8 @@ template <int GROUPS, int ALIGN, bool NIB = false>
 static cudaError_t launch_tile(const uint8_t* text, const uint8_t* pattern, size_t pitch,
                                long long n, int m, uint32_t* planes, uint32_t* err_flag,
                                cudaStream_t s) {
-    static bool attr = false;  // idempotent
-    if (!attr) {
-        cudaError_t st = cudaFuncSetAttribute(pack_tile_kernel<GROUPS, ALIGN, NIB>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              110 * 1024);
-        if (st != cudaSuccess) return st;
-        attr = true;
-    }
+    const cudaError_t st = ensure_smem_attr<pack_tile_kernel<GROUPS, ALIGN, NIB>>(110 * 1024);
+    if (st != cudaSuccess) return st;
     const long long ngroups = (n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + GROUPS - 1) / GROUPS);
     pack_tile_kernel<GROUPS, ALIGN, NIB><<<grid, kPackNT, tile_smem(pitch, GROUPS), s>>>(

@@ -185,13 +185,8 @@ cudaError_t launch_pack_planes(const uint64_t* text, const uint64_t* pattern, lo
         switch (w64) {
 #define SB_PP(W)                                                                               \
     case W: {                                                                                  \
-        static bool attr = false;                                                              \
-        if (!attr) {                                                                           \
-            const cudaError_t st = cudaFuncSetAttribute(                                       \
-                pack_planes_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-            if (st != cudaSuccess) return st;                                                  \
-            attr = true;                                                                       \
-        }                                                                                      \
+        const cudaError_t st = ensure_smem_attr<pack_planes_kernel<W>>(200 * 1024);            \
+        if (st != cudaSuccess) return st;                                                      \
         pack_planes_kernel<W><<<grid, 32 * kPackGroups, smem, s>>>(text, pattern, n, m, planes); \
         break;                                                                                 \
     }
