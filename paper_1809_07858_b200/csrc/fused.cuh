@@ -161,37 +161,46 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
         }
     } else {
         // D over columns tcol0 .. tcol0+B+2 rebuilt per block, pcol0 = tcol0 - E.
+        // The pattern columns of diagonal di are pcol0+di .. pcol0+di+X-1, held in
+        // a register ring: column pcol0+c sits in slot c % X. The diagonal loop
+        // runs in rolled chunks of X fully unrolled steps (slot indices stay
+        // compile-time, no register shuffling), so large E does not unroll into
+        // hundreds of hoisted loads.
         constexpr int X = B + 3;
         uint32_t T[X][3];
 #pragma unroll
         for (int x = 0; x < X; ++x) load_rel<CHECK, NC>(tbase, x, tcol0, m, T[x]);
         uint32_t P[X][3];
 #pragma unroll
-        for (int di = 0; di <= 2 * E; ++di) {
-            if (di == 0) {
+        for (int x = 0; x < X; ++x) load_rel<CHECK, NC>(pbase, x, pcol0, m, P[x]);
+        auto step = [&](const int rot, bool first) {
+            // rot = di % X: slot of pattern column pcol0 + di + x is (rot + x) % X
+            uint32_t sv[X];
 #pragma unroll
-                for (int x = 0; x < X; ++x) load_rel<CHECK, NC>(pbase, x, pcol0, m, P[x]);
-            } else {
-#pragma unroll
-                for (int x = 0; x < X - 1; ++x) {
-                    P[x][0] = P[x + 1][0];
-                    P[x][1] = P[x + 1][1];
-                    P[x][2] = P[x + 1][2];
-                }
-                load_rel<CHECK, NC>(pbase, X - 1 + di, pcol0, m, P[X - 1]);
+            for (int x = 0; x < X; ++x) {
+                const uint32_t* pp = P[(rot + x) % X];
+                sv[x] = (pp[0] ^ T[x][0]) | (pp[1] ^ T[x][1]) | pp[2] | T[x][2];
             }
-            uint32_t s[X];
-#pragma unroll
-            for (int x = 0; x < X; ++x)
-                s[x] = (P[x][0] ^ T[x][0]) | (P[x][1] ^ T[x][1]) | P[x][2] | T[x][2];
 #pragma unroll
             for (int b = 0; b < B; ++b) {
                 Cand4 cd;
-                make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
-                if (di == 0)
+                make_cand4(sv[b], sv[b + 1], sv[b + 2], sv[b + 3], cd);
+                if (first)
                     best[b] = cd;
                 else
                     update_best4(cd, best[b]);
+            }
+        };
+        step(0, true);  // di = 0
+#pragma unroll 1
+        for (int d0 = 1; d0 <= 2 * E; d0 += X) {
+#pragma unroll
+            for (int u = 0; u < X; ++u) {
+                const int di = d0 + u;
+                if (di > 2 * E) break;
+                // new column pcol0 + di + X - 1 replaces pcol0 + di - 1 in slot (di - 1) % X = u
+                load_rel<CHECK, NC>(pbase, di + X - 1, pcol0, m, P[u]);
+                step((1 + u) % X, false);
             }
         }
     }
