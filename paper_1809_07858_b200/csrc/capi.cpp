@@ -67,6 +67,9 @@ struct DeviceState {
     uint64_t* h_pk[2] = {nullptr, nullptr};
     size_t h_pk_words = 0;
     cudaEvent_t pk_ev[2] = {nullptr, nullptr};
+    // last use of the plane scratch (d_scratch, pipeline buffers) on any stream:
+    // device calls on caller streams and host batches on `stream` share them
+    cudaEvent_t scratch_ev = nullptr;
 };
 
 }  // namespace
@@ -123,7 +126,31 @@ long long pipeline_chunk() {
     return v;
 }
 
+// Order every use of the plane scratch after the previous one, whatever stream
+// each runs on (a device call on a caller stream may still be reading it when
+// the next call arrives on another stream).
+cudaError_t scratch_acquire(DeviceState& d, cudaStream_t s) {
+    if (!d.scratch_ev) {
+        const cudaError_t st = cudaEventCreateWithFlags(&d.scratch_ev, cudaEventDisableTiming);
+        if (st != cudaSuccess) return st;
+        return cudaSuccess;  // never recorded yet: nothing to wait for
+    }
+    return cudaStreamWaitEvent(s, d.scratch_ev, 0);
+}
+cudaError_t scratch_release(DeviceState& d, cudaStream_t s) {
+    return cudaEventRecord(d.scratch_ev, s);
+}
+
+cudaError_t launch_any_unordered(DeviceState& d, sb::FilterArgs a, cudaStream_t s);
+
 cudaError_t launch_any(DeviceState& d, sb::FilterArgs a, cudaStream_t s) {
+    cudaError_t st = scratch_acquire(d, s);
+    if (st == cudaSuccess) st = launch_any_unordered(d, a, s);
+    if (st == cudaSuccess) st = scratch_release(d, s);
+    return st;
+}
+
+cudaError_t launch_any_unordered(DeviceState& d, sb::FilterArgs a, cudaStream_t s) {
     const long long chunk = pipeline_chunk();
     if (sb::pipeline_applies(a, chunk)) {
         sb::Pipeline& p = d.pipe;
@@ -300,6 +327,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             return;
         const uint8_t* tsrc0 = text + p0 * stride;
         const uint8_t* psrc0 = pattern + p0 * stride;
+        if (!cu(scratch_acquire(d, d.stream), "scratch order")) return;
         const long long nchunks = (static_cast<long long>(n) + chunk - 1) / chunk;
         for (long long i = 0; i < nchunks; ++i) {
             const int b = static_cast<int>(i & 1);
@@ -340,6 +368,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             a.planes_words = d.scratch_words;
             if (!cu(sb::launch_filter(a, d.stream), "filter kernel")) return;
         }
+        if (!cu(scratch_release(d, d.stream), "scratch order")) return;
         if (!cu(xfer(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
                                 cudaMemcpyDeviceToHost, d.stream), "D2H accept"))
             return;
@@ -610,7 +639,10 @@ int pf_shouji_filter_nibbles_device(pf_ctx* ctx, const uint8_t* d_text, const ui
     a.estimates = d_estimates;
     a.planes = d.d_scratch;
     a.planes_words = d.scratch_words;
-    PF_CUDA(sb::launch_filter(a, static_cast<cudaStream_t>(stream)));
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PF_CUDA(scratch_acquire(d, s));
+    PF_CUDA(sb::launch_filter(a, s));
+    PF_CUDA(scratch_release(d, s));
     return PF_OK;
 }
 
@@ -663,6 +695,7 @@ void pf_ctx_destroy(pf_ctx* ctx) {
         cudaFree(d.d_bits);
         cudaFree(d.d_outplanes);
         cudaFree(d.d_scratch);
+        if (d.scratch_ev) cudaEventDestroy(d.scratch_ev);
         cudaFree(d.d_flag);
         cudaFree(d.d_key);
         cudaFree(d.d_stage);
@@ -757,6 +790,7 @@ void run_packed_shard(DeviceState& d, const uint64_t* text, const uint64_t* patt
                              size_t(m) * static_cast<size_t>((chunk + 31) / 32)),
                         "alloc tally planes"))
             return;
+        if (!cu(scratch_acquire(d, d.stream), "scratch order")) return;
         const long long nchunks = (static_cast<long long>(n) + chunk - 1) / chunk;
         for (long long i = 0; i < nchunks; ++i) {
             const int b = static_cast<int>(i & 1);
@@ -797,6 +831,7 @@ void run_packed_shard(DeviceState& d, const uint64_t* text, const uint64_t* patt
                             "bits"))
                 return;
         }
+        if (!cu(scratch_release(d, d.stream), "scratch order")) return;
     }
     if (!cu(xfer(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
                  cudaMemcpyDeviceToHost, d.stream), "D2H accept"))
@@ -1034,8 +1069,10 @@ int pf_shouji_filter_packed_device(pf_ctx* ctx, const uint64_t* d_text_planes,
     a.outplanes = d_bits ? d.d_outplanes : nullptr;
     a.planes = d.d_scratch;
     a.planes_words = d.scratch_words;
+    PF_CUDA(scratch_acquire(d, s));
     PF_CUDA(sb::launch_filter(a, s));
     if (d_bits) PF_CUDA(sb::launch_bits_transpose(d.d_outplanes, a.n, a.m, d_bits, s));
+    PF_CUDA(scratch_release(d, s));
     return PF_OK;
 }
 

@@ -399,3 +399,32 @@ def test_device_pitches(gpu, oracle, m, pitch):
                                         estimates=True)
     a2, e2, _ = oracle.shouji_batch(t, p, 5)
     assert (a1 == a2).all() and (e1 == e2).all()
+
+
+def test_device_calls_on_two_streams_share_scratch_safely(gpu):
+    """Async device calls of one context on two different streams, back to back: the
+    context's plane scratch is reused, so the second call must wait for the first
+    (event ordering inside the library) — both results must equal serial runs."""
+    import torch
+    n, m = 4_000_000, 100
+    pitch = gpu.device_pitch(m)
+    data = []
+    for k, e in ((1, 5), (2, 3)):
+        tt = torch.empty((n, pitch), dtype=torch.uint8, device="cuda")
+        pt = torch.empty((n, pitch), dtype=torch.uint8, device="cuda")
+        gpu.generate_device(1, 500 + k, e, tt.data_ptr(), pt.data_ptr(), pitch, n, m)
+        ref = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+        gpu.shouji_filter_device(tt.data_ptr(), pt.data_ptr(), pitch, n, m, e, ref.data_ptr())
+        data.append((tt, pt, e, ref))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for (tt, pt, e, _), st in zip(data, streams):
+        acc = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        gpu.shouji_filter_device_async(tt.data_ptr(), pt.data_ptr(), pitch, n, m, e,
+                                       acc.data_ptr(), flag.data_ptr(), stream=st.cuda_stream)
+        outs.append(acc)
+    torch.cuda.synchronize()
+    for (_, _, _, ref), acc in zip(data, outs):
+        assert torch.equal(acc, ref)
