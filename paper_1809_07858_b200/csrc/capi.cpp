@@ -53,8 +53,6 @@ struct DeviceState {
     uint8_t* h_stage[2] = {nullptr, nullptr};
     size_t stage_bytes = 0;
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
-    sb::Pipeline pipe;           // pack/search overlap for large batches
-    size_t pipe_words[2] = {0, 0};
     // host-pack upload path: pinned nibble buffers, device nibble buffers, events
     uint8_t* h_nib[2] = {nullptr, nullptr};
     size_t h_nib_bytes = 0;
@@ -67,7 +65,7 @@ struct DeviceState {
     uint64_t* h_pk[2] = {nullptr, nullptr};
     size_t h_pk_words = 0;
     cudaEvent_t pk_ev[2] = {nullptr, nullptr};
-    // last use of the plane scratch (d_scratch, pipeline buffers) on any stream:
+    // last use of the plane scratch (d_scratch) on any stream:
     // device calls on caller streams and host batches on `stream` share them
     cudaEvent_t scratch_ev = nullptr;
 };
@@ -113,19 +111,7 @@ cudaError_t grow(T*& p, size_t& have, size_t need) {
     return st;
 }
 
-// Allocate plane scratch and launch: large fused batches go through the
-// chunked two-stream pipeline, everything else through a single pack+search.
-// Pairs per pipeline chunk (multiple of 256); 0 disables the pipeline.
-// PF_PIPELINE_CHUNK overrides the default (experiments / tuning).
-long long pipeline_chunk() {
-    static const long long v = [] {
-        const char* e = std::getenv("PF_PIPELINE_CHUNK");
-        long long c = e ? std::atoll(e) : sb::kPipelineChunk;
-        return c > 0 ? (c + 255) / 256 * 256 : 0;
-    }();
-    return v;
-}
-
+// Allocate plane scratch and launch pack + search.
 // Order every use of the plane scratch after the previous one, whatever stream
 // each runs on (a device call on a caller stream may still be reading it when
 // the next call arrives on another stream).
@@ -151,24 +137,7 @@ cudaError_t launch_any(DeviceState& d, sb::FilterArgs a, cudaStream_t s) {
 }
 
 cudaError_t launch_any_unordered(DeviceState& d, sb::FilterArgs a, cudaStream_t s) {
-    const long long chunk = pipeline_chunk();
-    if (sb::pipeline_applies(a, chunk)) {
-        sb::Pipeline& p = d.pipe;
-        cudaError_t st = cudaSuccess;
-        if (!p.side) st = cudaStreamCreateWithFlags(&p.side, cudaStreamNonBlocking);
-        cudaEvent_t* evs[] = {&p.start, &p.done, &p.packed[0], &p.packed[1], &p.searched[0],
-                              &p.searched[1]};
-        for (cudaEvent_t* e : evs)
-            if (st == cudaSuccess && !*e) st = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
-        const size_t need = sb::planes_scratch_words(chunk, a.m);
-        for (int b = 0; b < 2 && st == cudaSuccess; ++b) st = grow(p.planes[b], d.pipe_words[b], need);
-        if (st != cudaSuccess) return st;
-        p.planes_words = std::min(d.pipe_words[0], d.pipe_words[1]);
-        p.chunk = chunk;
-        return sb::launch_filter_pipelined(a, p, s);
-    }
-    cudaError_t st = grow(d.d_scratch, d.scratch_words,
-                          sb::planes_scratch_words(a.n, a.m));
+    const cudaError_t st = grow(d.d_scratch, d.scratch_words, sb::planes_scratch_words(a.n, a.m));
     if (st != cudaSuccess) return st;
     a.planes = d.d_scratch;
     a.planes_words = d.scratch_words;
@@ -707,13 +676,6 @@ void pf_ctx_destroy(pf_ctx* ctx) {
             cudaFree(d.d_pk[b]);
             if (d.pk_ev[b]) cudaEventDestroy(d.pk_ev[b]);
         }
-        cudaFree(d.pipe.planes[0]);
-        cudaFree(d.pipe.planes[1]);
-        cudaEvent_t evs[] = {d.pipe.start, d.pipe.done, d.pipe.packed[0], d.pipe.packed[1],
-                             d.pipe.searched[0], d.pipe.searched[1]};
-        for (cudaEvent_t e : evs)
-            if (e) cudaEventDestroy(e);
-        if (d.pipe.side) cudaStreamDestroy(d.pipe.side);
         for (int b = 0; b < 2; ++b) {
             if (d.h_stage[b]) cudaFreeHost(d.h_stage[b]);
             if (d.stage_ev[b]) cudaEventDestroy(d.stage_ev[b]);

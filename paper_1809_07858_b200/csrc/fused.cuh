@@ -487,38 +487,6 @@ shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
     search_group<E, true>(planes, g, n, m, accept, estimates, outplanes);
 }
 
-// Pack + search in one kernel: a CTA packs the planes of its 128 groups
-// (4096 pairs; TMA tiles, pack_tile.cuh) into the planes array, then each
-// thread sweeps one group. Different CTAs on an SM sit in different phases,
-// so the memory-bound packing of one overlaps the integer-bound search of
-// another; the planes a CTA reads back were written moments before (L2).
-constexpr int kFusedNT = 128;
-
-template <int E>
-__global__ void __launch_bounds__(kFusedNT)
-shouji_fused_w4(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern, size_t pitch,
-                long long n, int m, int tile_groups, uint32_t* __restrict__ planes,
-                uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
-                uint32_t* __restrict__ err_flag) {
-    extern __shared__ __align__(128) uint8_t sm[];
-    __shared__ __align__(8) uint64_t bar;
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
-    __syncthreads();
-    const long long ngroups = (n + 31) / 32;
-    const long long gbase = static_cast<long long>(blockIdx.x) * kFusedNT;
-    uint32_t err = 0u, parity = 0u;
-    for (int t = 0; t < kFusedNT / tile_groups; ++t) {
-        const long long g0 = gbase + static_cast<long long>(t) * tile_groups;
-        if (g0 >= ngroups) break;
-        err |= pack_one_tile<4, kFusedNT>(sm, &bar, parity, tile_groups, g0, text, pattern, pitch, n,
-                                          m, planes);
-        parity ^= 1u;
-    }
-    if (err) atomicOr(err_flag, 1u);
-    __syncthreads();  // this CTA's planes are written (CTA-scope ordering)
-    search_group<E, false>(planes, gbase + threadIdx.x, n, m, accept, estimates, nullptr);
-}
-
 template <int E>
 cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s) {
     using Cfg = SearchCfg<E>;
@@ -545,23 +513,8 @@ cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int E>
-cudaError_t launch_fused_e(const FilterArgs& a, cudaStream_t s) {
-    const int groups = tile_groups(a.pitch);
-    const size_t smem = tile_smem(a.pitch, groups);
-    const cudaError_t st = ensure_smem_attr<shouji_fused_w4<E>>(110 * 1024);
-    if (st != cudaSuccess) return st;
-    const long long ngroups = (a.n + 31) / 32;
-    const unsigned grid = static_cast<unsigned>((ngroups + kFusedNT - 1) / kFusedNT);
-    shouji_fused_w4<E><<<grid, kFusedNT, smem, s>>>(a.text, a.pattern, a.pitch, a.n, a.m, groups,
-                                                     a.planes, a.accept, a.estimates, a.err_flag);
-    count_launch();
-    return cudaGetLastError();
-}
-
 }  // namespace sb
 
 // Explicit instantiation helper for the fused_e*.cu units.
 #define SB_INSTANTIATE_FUSED(E)                                                      \
-    template cudaError_t sb::launch_search_e<E>(const sb::FilterArgs&, cudaStream_t); \
-    template cudaError_t sb::launch_fused_e<E>(const sb::FilterArgs&, cudaStream_t);
+    template cudaError_t sb::launch_search_e<E>(const sb::FilterArgs&, cudaStream_t);

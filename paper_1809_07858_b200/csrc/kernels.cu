@@ -222,38 +222,20 @@ __global__ void accept_all(long long n, int m, uint32_t* accept, uint32_t* estim
 // parallel: each E is its own fully unrolled kernel).
 template <int E>
 cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s);
-template <int E>
-cudaError_t launch_fused_e(const FilterArgs& a, cudaStream_t s);
 
 using SearchFn = cudaError_t (*)(const FilterArgs&, cudaStream_t);
 template <int... Es>
 static constexpr std::array<SearchFn, sizeof...(Es)> make_search_table(std::integer_sequence<int, Es...>) {
     return {&launch_search_e<Es>...};
 }
-template <int... Es>
-static constexpr std::array<SearchFn, sizeof...(Es)> make_fused_table(std::integer_sequence<int, Es...>) {
-    return {&launch_fused_e<Es>...};
-}
 static constexpr auto kSearchTable =
     make_search_table(std::make_integer_sequence<int, kFusedMaxE + 1>{});
-static constexpr auto kFusedTable =
-    make_fused_table(std::make_integer_sequence<int, kFusedMaxE + 1>{});
 
-// One-kernel pack+search (shouji_fused_w4) only when PF_FUSED=1: measured
-// slower than pack + search on B200 (profiles/r1_notes.md), kept for A/B runs.
 // Prefetching search (fused.cuh shouji_search_w4_pf): PF_SEARCH_PF=0 turns it off.
 bool search_prefetch_enabled() {
     static const bool v = [] {
         const char* e = std::getenv("PF_SEARCH_PF");
         return !(e && e[0] == '0');
-    }();
-    return v;
-}
-
-static bool fused_enabled() {
-    static const bool v = [] {
-        const char* e = std::getenv("PF_FUSED");
-        return e && e[0] == '1';
     }();
     return v;
 }
@@ -290,10 +272,6 @@ bool use_fused(uint32_t width, uint32_t e, int m) {
 cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
     if (a.n <= 0) return cudaSuccess;
     if (a.planes == nullptr || a.planes_words < plane_words(a.n, a.m)) return cudaErrorInvalidValue;
-    const bool tile_ok = tile_smem(a.pitch, tile_groups(a.pitch)) <= 110 * 1024 && a.pitch % 4 == 0;
-    if (!a.nibbles && !a.packed_text && use_fused(a.width, a.e, a.m) && tile_ok &&
-        a.outplanes == nullptr && fused_enabled())
-        return kFusedTable[a.e](a, s);
     cudaError_t st =
         a.packed_text ? launch_pack_planes(a.packed_text, a.packed_pattern, a.n, a.m, a.planes, s)
         : a.nibbles   ? launch_pack_nibbles(a.text, a.pattern, a.n, a.m, a.planes, s)
@@ -301,43 +279,6 @@ cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
     if (st != cudaSuccess) return st;
     if (use_fused(a.width, a.e, a.m)) return kSearchTable[a.e](a, s);
     return a.m <= 255 ? launch_generic<8>(a, s) : launch_generic<24>(a, s);
-}
-
-bool pipeline_applies(const FilterArgs& a, long long chunk) {
-    return chunk > 0 && a.n > chunk && a.outplanes == nullptr && !a.nibbles && !a.packed_text &&
-           use_fused(a.width, a.e, a.m);
-}
-
-cudaError_t launch_filter_pipelined(const FilterArgs& a, const Pipeline& p, cudaStream_t s) {
-    const long long chunk = p.chunk;
-    if (chunk % 256 != 0 || p.planes_words < plane_words(chunk, a.m)) return cudaErrorInvalidValue;
-    cudaError_t st = cudaEventRecord(p.start, s);
-    if (st == cudaSuccess) st = cudaStreamWaitEvent(p.side, p.start, 0);
-    const long long nchunks = (a.n + chunk - 1) / chunk;
-    for (long long i = 0; i < nchunks && st == cudaSuccess; ++i) {
-        const int buf = static_cast<int>(i & 1);
-        const long long lo = i * chunk;
-        const long long cn = (a.n - lo < chunk) ? a.n - lo : chunk;
-        // buffer reuse: the search of chunk i-2 must be done reading it
-        if (i >= 2) st = cudaStreamWaitEvent(s, p.searched[buf], 0);
-        if (st != cudaSuccess) break;
-        st = launch_pack(a.text + lo * a.pitch, a.pattern + lo * a.pitch, a.pitch, cn, a.m,
-                         p.planes[buf], a.err_flag, s);
-        if (st == cudaSuccess) st = cudaEventRecord(p.packed[buf], s);
-        if (st == cudaSuccess) st = cudaStreamWaitEvent(p.side, p.packed[buf], 0);
-        if (st != cudaSuccess) break;
-        FilterArgs c = a;
-        c.n = cn;
-        c.planes = p.planes[buf];
-        c.planes_words = p.planes_words;
-        c.accept = a.accept + lo / 32;
-        c.estimates = a.estimates ? a.estimates + lo : nullptr;
-        st = kSearchTable[a.e](c, p.side);
-        if (st == cudaSuccess) st = cudaEventRecord(p.searched[buf], p.side);
-    }
-    if (st == cudaSuccess) st = cudaEventRecord(p.done, p.side);
-    if (st == cudaSuccess) st = cudaStreamWaitEvent(s, p.done, 0);
-    return st;
 }
 
 cudaError_t launch_validate(const FilterArgs& a, cudaStream_t s) {

@@ -64,23 +64,6 @@ cudaError_t launch_pack_planes(const uint64_t* text, const uint64_t* pattern, lo
                                uint32_t* planes, cudaStream_t s);
 // Launch the filter (pack + width-4 search, or pack + generic). Returns a cudaError_t.
 cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s);
-// Resources for the chunked, two-stream pipeline: pack of chunk i+1 (memory
-// bound) runs on the caller's stream while the search of chunk i (integer
-// bound) runs on `side`; two plane buffers alternate.
-struct Pipeline {
-    cudaStream_t side = nullptr;
-    cudaEvent_t start = nullptr, done = nullptr;
-    cudaEvent_t packed[2] = {nullptr, nullptr};
-    cudaEvent_t searched[2] = {nullptr, nullptr};
-    uint32_t* planes[2] = {nullptr, nullptr};
-    size_t planes_words = 0;  // capacity of each buffer
-    long long chunk = 0;      // pairs per chunk (multiple of 256)
-};
-constexpr long long kPipelineChunk = 0;  // default: off (see capi.cpp pipeline_chunk)
-
-// Whether launch_filter_pipelined applies (fused width-4 path, no tally dump, n > one chunk).
-bool pipeline_applies(const FilterArgs& a, long long chunk);
-cudaError_t launch_filter_pipelined(const FilterArgs& a, const Pipeline& p, cudaStream_t s);
 // Validation only (for e >= m or an invalid width): sets *err_flag on any illegal byte.
 cudaError_t launch_validate(const FilterArgs& a, cudaStream_t s);
 // First illegal byte: key = ((pair*2+field) << 24) | pos into *d_key (pre-set to ~0).

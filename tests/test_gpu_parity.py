@@ -335,10 +335,10 @@ def test_pinned_host_buffers(gpu, oracle):
     assert (a == a2).all() and (e == e2).all()
 
 
-# --- large batches: the chunked two-stream pipeline equals one-chunk launches -------
+# --- large batches: one launch equals the same pairs in 1Mi-pair sub-batches --------
 
 @pytest.mark.parametrize("n", [2 * 1048576 + 1, 5 * 1048576 + 37])
-def test_pipelined_large_batch(gpu, oracle, n):
+def test_large_batch_equals_sub_batches(gpu, oracle, n):
     import torch
     m, e = 100, 5
     pitch = gpu.device_pitch(m)
