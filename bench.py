@@ -373,8 +373,8 @@ def run_ours(args, rank, world, local_rank):
                "ascii_bytes_per_step": int(2 * n * m),
                "ms_per_step": 1e3 * e2e_s,
                "path": "pf_shouji_filter_batch(pinned host ASCII records, stride=m): host cores pack "
-                       "nibble records chunk by chunk into pinned buffers, H2D, device pack + search "
-                       "kernels, D2H accept bitmap, sync"
+                       "2-bit dibit records (N planes only for chunks with an N) chunk by chunk into "
+                       "pinned buffers, H2D, device pack + search kernels, D2H accept bitmap, sync"
                        if (x1[0] - x0[0]) < 2 * n * m * args.steps else
                        "pf_shouji_filter_batch(pinned host ASCII records, stride=m) -> H2D, "
                        "pack + search kernels, D2H accept bitmap, sync"}

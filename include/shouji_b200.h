@@ -169,6 +169,26 @@ int pf_shouji_filter_one(pf_ctx* ctx, const char* pattern, size_t pattern_len, c
                          size_t text_len, uint32_t e, uint32_t width, int* accept,
                          uint32_t* estimate, uint64_t* bits, pf_error* err);
 
+/* Dibit records: the default upload format of the host-pack path (2 bits per
+ * base; pf_dibit_pitch(m) = 4*ceil(m/16) bytes per record: byte q of 32-bit
+ * word w holds the codes (ASCII bits 1-2) of columns 16w+q, +4, +8, +12 at
+ * bits 0-1, 2-3, 4-5, 6-7). N is carried in N-plane records
+ * (pf_nplane_pitch(m) = 4*ceil(m/32) bytes, bit c = column c is 'N'), written
+ * by pf_host_pack_dibits only when *has_n comes back 1 (both N arrays may be
+ * NULL when the caller knows there is no N). pf_shouji_filter_dibits_device
+ * filters dibit records on the device; pass NULL N arrays for N-free batches.
+ * PF_HOST_FORMAT=nibble makes pf_shouji_filter_batch upload nibbles instead. */
+size_t pf_dibit_pitch(uint32_t m);
+size_t pf_nplane_pitch(uint32_t m);
+int pf_host_pack_dibits(const uint8_t* text, const uint8_t* pattern, size_t stride, size_t n,
+                        uint32_t m, uint8_t* out_text, uint8_t* out_pattern, uint8_t* n_text,
+                        uint8_t* n_pattern, int* has_n, int simd, pf_error* err);
+int pf_shouji_filter_dibits_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                                   const uint8_t* d_ntext, const uint8_t* d_npattern, size_t n,
+                                   uint32_t m, uint32_t e, uint32_t width,
+                                   uint32_t* d_accept_bitmap, uint32_t* d_estimates, void* stream,
+                                   pf_error* err);
+
 /* ---- Packed-planes variant --------------------------------
  * Pairs the caller already packed with packed_sequence::from_string
  * (proj/src/packed_sequence.cpp:7-34), passed in that class's own storage:

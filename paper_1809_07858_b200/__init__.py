@@ -43,6 +43,10 @@ from .api import (  # noqa: F401
     magnet_filter_batch,
     magnet_filter_device,
     nibble_pitch,
+    dibit_pitch,
+    nplane_pitch,
+    host_pack_dibits,
+    shouji_filter_dibits_device,
     host_pack_nibbles,
     shouji_filter_nibbles_device,
     threshold_too_large_error,

@@ -36,7 +36,8 @@ EXPORTED = [
     "pf_dataset_size", "pf_dataset_length", "pf_dataset_text", "pf_dataset_pattern",
     "pf_dataset_source", "pf_dataset_write_tsv", "pf_dataset_free", "pf_banded_edit_distance_batch",
     "pf_nibble_pitch", "pf_host_pack_nibbles", "pf_shouji_filter_nibbles_device",
-    "pf_transfer_bytes", "pf_magnet_filter_batch", "pf_magnet_filter_device",
+    "pf_transfer_bytes", "pf_dibit_pitch", "pf_nplane_pitch", "pf_host_pack_dibits",
+    "pf_shouji_filter_dibits_device", "pf_magnet_filter_batch", "pf_magnet_filter_device",
     "pf_magnet_filter_one", "pf_packed_words", "pf_shouji_filter_packed_batch",
     "pf_shouji_filter_packed_device",
 ]
@@ -100,6 +101,12 @@ def _bind(lib):
         "pf_banded_edit_distance_batch": (C.c_int, [_vp, _vp, _vp, _sz, _sz, _u32, _u32, _vp,
                                                     C.POINTER(PfError)]),
         "pf_nibble_pitch": (_sz, [_u32]),
+        "pf_dibit_pitch": (_sz, [_u32]),
+        "pf_nplane_pitch": (_sz, [_u32]),
+        "pf_host_pack_dibits": (C.c_int, [_vp, _vp, _sz, _sz, _u32, _vp, _vp, _vp, _vp,
+                                          C.POINTER(C.c_int), C.c_int, C.POINTER(PfError)]),
+        "pf_shouji_filter_dibits_device": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _sz, _u32, _u32,
+                                                     _u32, _vp, _vp, _vp, C.POINTER(PfError)]),
         "pf_transfer_bytes": (None, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "pf_packed_words": (_sz, [_u32]),
         "pf_shouji_filter_packed_batch": (C.c_int, [_vp, _vp, _vp, _sz, _u32, _u32, _u32, _vp, _vp,

@@ -516,6 +516,53 @@ def host_pack_nibbles(text, pattern, m: int | None = None, simd: bool = True):
     return ot, op
 
 
+def dibit_pitch(m: int) -> int:
+    """Bytes per dibit record of length m (4 * ceil(m / 16))."""
+    return int(L.lib.pf_dibit_pitch(int(m)))
+
+
+def nplane_pitch(m: int) -> int:
+    """Bytes per N-plane record of length m (4 * ceil(m / 32))."""
+    return int(L.lib.pf_nplane_pitch(int(m)))
+
+
+def host_pack_dibits(text, pattern, m: int | None = None, simd: bool = True):
+    """Host upload stage in the default format: ASCII records -> dibit records and
+    N-plane records (the latter None when no base is N), validated like
+    packed_sequence::from_string. Returns (dib_text, dib_pattern, n_text, n_pattern)."""
+    text = _as_records(text)
+    pattern = _as_records(pattern)
+    if text.shape != pattern.shape:
+        raise length_mismatch_error("text and pattern record arrays differ in shape")
+    n, stride = text.shape
+    m = stride if m is None else int(m)
+    dt = np.zeros((n, dibit_pitch(m)), np.uint8)
+    dq = np.zeros((n, dibit_pitch(m)), np.uint8)
+    nt = np.zeros((n, nplane_pitch(m)), np.uint8)
+    nq = np.zeros((n, nplane_pitch(m)), np.uint8)
+    has_n = C.c_int()
+    err = L.PfError()
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    st = L.lib.pf_host_pack_dibits(ptr(text), ptr(pattern), stride, n, m, ptr(dt), ptr(dq), ptr(nt),
+                                   ptr(nq), C.byref(has_n), 1 if simd else 0, C.byref(err))
+    _raise(st, err)
+    return (dt, dq, nt, nq) if has_n.value else (dt, dq, None, None)
+
+
+def shouji_filter_dibits_device(d_text: int, d_pattern: int, n: int, m: int, e: int,
+                                d_accept: int, d_ntext: int | None = None,
+                                d_npattern: int | None = None, width: int = default_window_width,
+                                d_estimates: int | None = None, stream: int | None = None,
+                                ctx: Context | None = None) -> None:
+    """Filter dibit records (+ optional N-plane records) already on the device."""
+    ctx = ctx or default_context()
+    err = L.PfError()
+    st = L.lib.pf_shouji_filter_dibits_device(ctx.handle, d_text, d_pattern, d_ntext, d_npattern,
+                                              n, m, int(e), int(width), d_accept, d_estimates,
+                                              stream, C.byref(err))
+    _raise(st, err)
+
+
 def shouji_filter_nibbles_device(d_text: int, d_pattern: int, n: int, m: int, e: int,
                                  d_accept: int, width: int = default_window_width,
                                  d_estimates: int | None = None, stream: int | None = None,

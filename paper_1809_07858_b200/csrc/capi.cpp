@@ -59,6 +59,10 @@ struct DeviceState {
     uint8_t* d_nib[2] = {nullptr, nullptr};
     size_t d_nib_bytes[2] = {0, 0};
     cudaEvent_t nib_ev[2] = {nullptr, nullptr};
+    uint8_t* h_nrow[2] = {nullptr, nullptr};  // dibit path: pinned N-plane rows
+    size_t h_nrow_bytes = 0;
+    uint8_t* d_nrow[2] = {nullptr, nullptr};
+    size_t d_nrow_bytes[2] = {0, 0};
     // packed-planes input: device chunk buffers (text, pattern) and pinned staging
     uint64_t* d_pk[2] = {nullptr, nullptr};
     size_t d_pk_words[2] = {0, 0};
@@ -173,6 +177,17 @@ int host_pack_mode() {
 }
 constexpr long long kHostPackMin = 1ll << 16;
 
+// Upload format of the host-pack path: dibit records (2 bits per base, N
+// planes only for chunks that contain an N; default) or nibble records
+// (4 bits per base). PF_HOST_FORMAT=nibble selects the latter.
+bool host_format_dibit() {
+    static const bool v = [] {
+        const char* e = std::getenv("PF_HOST_FORMAT");
+        return !(e && std::strcmp(e, "nibble") == 0);
+    }();
+    return v;
+}
+
 // Pairs per host-pack chunk (PF_HOST_CHUNK overrides; multiple of 256).
 long long host_chunk() {
     static const long long v = [] {
@@ -242,7 +257,8 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     };
     const int hp_mode = host_pack_mode();
     const bool host_pack = hp_mode != 0 && !dist && !magnet && e < m && width >= 3 && width <= 8 && !bits &&
-                           sb::nibble_pack_fits(static_cast<int>(m)) &&
+                           (host_format_dibit() ? sb::dibit_pack_fits(static_cast<int>(m))
+                                                : sb::nibble_pack_fits(static_cast<int>(m))) &&
                            (hp_mode == 1 || static_cast<long long>(n) >= kHostPackMin);
     if (!host_pack) {
         if (!cu(grow(d.d_text, d.in_bytes, n * pitch), "alloc text")) return;
@@ -268,12 +284,15 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     // the bytes) chunk by chunk into pinned buffers; chunk i's DMA, device pack
     // and search run on the stream while the cores pack chunk i+1.
     if (host_pack) {
-        // pairs per chunk; a multiple of 256 so the pattern rows (at chunk * np)
-        // stay 16-byte aligned for the pack kernel's bulk copies
+        const bool dib = host_format_dibit();
+        // pairs per chunk; a multiple of 256 so the pattern rows (at chunk * rp)
+        // stay 16-byte aligned for the pack kernels' bulk copies
         const long long chunk =
             std::min<long long>((static_cast<long long>(n) + 255) / 256 * 256, host_chunk());
-        const size_t np = sb::nibble_pitch(static_cast<int>(m));
-        const size_t cbytes = 2 * static_cast<size_t>(chunk) * np;  // text rows, then pattern rows
+        const size_t rp = dib ? sb::dibit_pitch(static_cast<int>(m)) : sb::nibble_pitch(static_cast<int>(m));
+        const size_t npr = sb::nplane_pitch(static_cast<int>(m));
+        const size_t cbytes = 2 * static_cast<size_t>(chunk) * rp;  // text rows, then pattern rows
+        const size_t nbytes = dib ? 2 * static_cast<size_t>(chunk) * npr : 0;
         if (d.h_nib_bytes < cbytes) {
             for (int b = 0; b < 2; ++b) {
                 if (d.h_nib[b]) cudaFreeHost(d.h_nib[b]);
@@ -281,12 +300,24 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             }
             d.h_nib_bytes = 0;
             for (int b = 0; b < 2; ++b)
-                if (!cu(cudaHostAlloc(&d.h_nib[b], cbytes, cudaHostAllocPortable), "alloc host nibbles"))
+                if (!cu(cudaHostAlloc(&d.h_nib[b], cbytes, cudaHostAllocPortable), "alloc host records"))
                     return;
             d.h_nib_bytes = cbytes;
         }
+        if (d.h_nrow_bytes < nbytes) {
+            for (int b = 0; b < 2; ++b) {
+                if (d.h_nrow[b]) cudaFreeHost(d.h_nrow[b]);
+                d.h_nrow[b] = nullptr;
+            }
+            d.h_nrow_bytes = 0;
+            for (int b = 0; b < 2; ++b)
+                if (!cu(cudaHostAlloc(&d.h_nrow[b], nbytes, cudaHostAllocPortable), "alloc host N rows"))
+                    return;
+            d.h_nrow_bytes = nbytes;
+        }
         for (int b = 0; b < 2; ++b) {
-            if (!cu(grow(d.d_nib[b], d.d_nib_bytes[b], cbytes), "alloc device nibbles")) return;
+            if (!cu(grow(d.d_nib[b], d.d_nib_bytes[b], cbytes), "alloc device records")) return;
+            if (dib && !cu(grow(d.d_nrow[b], d.d_nrow_bytes[b], nbytes), "alloc device N rows")) return;
             if (!d.nib_ev[b] &&
                 !cu(cudaEventCreateWithFlags(&d.nib_ev[b], cudaEventDisableTiming), "event"))
                 return;
@@ -302,31 +333,49 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             const int b = static_cast<int>(i & 1);
             const long long lo = i * chunk;
             const long long cn = std::min<long long>(chunk, static_cast<long long>(n) - lo);
-            // the DMA that last read this pinned buffer (chunk i-2) must be done
-            if (i >= 2 && !cu(cudaEventSynchronize(d.nib_ev[b]), "nibble buffer wait")) return;
+            // the DMA that last read these pinned buffers (chunk i-2) must be done
+            if (i >= 2 && !cu(cudaEventSynchronize(d.nib_ev[b]), "record buffer wait")) return;
             uint8_t* ht = d.h_nib[b];
-            uint8_t* hq = ht + static_cast<size_t>(chunk) * np;
+            uint8_t* hq = ht + static_cast<size_t>(chunk) * rp;
+            uint8_t* hnt = dib ? d.h_nrow[b] : nullptr;
+            uint8_t* hnq = dib ? d.h_nrow[b] + static_cast<size_t>(chunk) * npr : nullptr;
             sb::HostBad bad;
-            sb::host_pack_nibbles_parallel(tsrc0 + lo * stride, psrc0 + lo * stride, stride, cn,
-                                           static_cast<int>(m), ht, hq, &bad);
+            bool has_n = false;
+            if (dib)
+                sb::host_pack_dibits_parallel(tsrc0 + lo * stride, psrc0 + lo * stride, stride, cn,
+                                              static_cast<int>(m), ht, hq, hnt, hnq, &bad, &has_n);
+            else
+                sb::host_pack_nibbles_parallel(tsrc0 + lo * stride, psrc0 + lo * stride, stride, cn,
+                                               static_cast<int>(m), ht, hq, &bad);
             if (bad.any) {  // chunks run in pair order: the first chunk with a bad byte wins
                 cu(cudaStreamSynchronize(d.stream), "sync");
                 set_illegal(err, p0 + lo + bad.pair, static_cast<uint32_t>(bad.field),
                             static_cast<uint64_t>(bad.pos), bad.byte);
                 return fail(PF_ERR_ILLEGAL_CHARACTER);
             }
-            const size_t cb = static_cast<size_t>(cn) * np;
-            if (!cu(xfer(d.d_nib[b], ht, cb, cudaMemcpyHostToDevice, d.stream), "H2D nibbles"))
+            const size_t cb = static_cast<size_t>(cn) * rp;
+            if (!cu(xfer(d.d_nib[b], ht, cb, cudaMemcpyHostToDevice, d.stream), "H2D records"))
                 return;
-            if (!cu(xfer(d.d_nib[b] + static_cast<size_t>(chunk) * np, hq, cb,
-                         cudaMemcpyHostToDevice, d.stream), "H2D nibbles"))
+            if (!cu(xfer(d.d_nib[b] + static_cast<size_t>(chunk) * rp, hq, cb,
+                         cudaMemcpyHostToDevice, d.stream), "H2D records"))
                 return;
-            if (!cu(cudaEventRecord(d.nib_ev[b], d.stream), "nibble record")) return;
+            if (has_n) {
+                const size_t nb = static_cast<size_t>(cn) * npr;
+                if (!cu(xfer(d.d_nrow[b], hnt, nb, cudaMemcpyHostToDevice, d.stream), "H2D N rows"))
+                    return;
+                if (!cu(xfer(d.d_nrow[b] + static_cast<size_t>(chunk) * npr, hnq, nb,
+                             cudaMemcpyHostToDevice, d.stream), "H2D N rows"))
+                    return;
+            }
+            if (!cu(cudaEventRecord(d.nib_ev[b], d.stream), "record event")) return;
             sb::FilterArgs a{};
             a.text = d.d_nib[b];
-            a.pattern = d.d_nib[b] + static_cast<size_t>(chunk) * np;
-            a.pitch = np;
-            a.nibbles = true;
+            a.pattern = d.d_nib[b] + static_cast<size_t>(chunk) * rp;
+            a.pitch = rp;
+            a.nibbles = !dib;
+            a.dibits = dib;
+            a.ntext = has_n ? d.d_nrow[b] : nullptr;
+            a.npattern = has_n ? d.d_nrow[b] + static_cast<size_t>(chunk) * npr : nullptr;
             a.n = cn;
             a.m = static_cast<int>(m);
             a.e = e;
@@ -615,6 +664,84 @@ int pf_shouji_filter_nibbles_device(pf_ctx* ctx, const uint8_t* d_text, const ui
     return PF_OK;
 }
 
+size_t pf_dibit_pitch(uint32_t m) { return sb::dibit_pitch(static_cast<int>(std::max<uint32_t>(m, 1))); }
+size_t pf_nplane_pitch(uint32_t m) { return sb::nplane_pitch(static_cast<int>(std::max<uint32_t>(m, 1))); }
+
+int pf_host_pack_dibits(const uint8_t* text, const uint8_t* pattern, size_t stride, size_t n,
+                        uint32_t m, uint8_t* out_text, uint8_t* out_pattern, uint8_t* n_text,
+                        uint8_t* n_pattern, int* has_n, int simd, pf_error* err) {
+    if (err) std::memset(err, 0, sizeof(*err));
+    if (has_n) *has_n = 0;
+    if (n == 0) return PF_OK;
+    if (!text || !pattern || !out_text || !out_pattern || !has_n) return PF_ERR_NULL_ARGUMENT;
+    if (m == 0) {
+        set_err(err, PF_ERR_EMPTY_SEQUENCE, "empty sequence");
+        return PF_ERR_EMPTY_SEQUENCE;
+    }
+    if (stride < m) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS, "stride < m");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    sb::HostBad bad;
+    bool any = false;
+    sb::host_pack_dibits_parallel(text, pattern, stride, static_cast<long long>(n),
+                                  static_cast<int>(m), out_text, out_pattern, n_text, n_pattern,
+                                  &bad, &any, simd != 0);
+    if (bad.any) {
+        set_illegal(err, bad.pair, static_cast<uint32_t>(bad.field), static_cast<uint64_t>(bad.pos),
+                    bad.byte);
+        return PF_ERR_ILLEGAL_CHARACTER;
+    }
+    *has_n = any ? 1 : 0;
+    return PF_OK;
+}
+
+int pf_shouji_filter_dibits_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                                   const uint8_t* d_ntext, const uint8_t* d_npattern, size_t n,
+                                   uint32_t m, uint32_t e, uint32_t width,
+                                   uint32_t* d_accept_bitmap, uint32_t* d_estimates, void* stream,
+                                   pf_error* err) {
+    if (err) std::memset(err, 0, sizeof(*err));
+    if (!ctx) return PF_ERR_NULL_ARGUMENT;
+    if (n == 0) return PF_OK;
+    if (!d_text || !d_pattern || !d_accept_bitmap || (!d_ntext != !d_npattern))
+        return PF_ERR_NULL_ARGUMENT;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(d_text) | reinterpret_cast<uintptr_t>(d_pattern) |
+                         reinterpret_cast<uintptr_t>(d_ntext) | reinterpret_cast<uintptr_t>(d_npattern);
+    if (m == 0 || e >= m || width < 3 || width > 8 || !sb::dibit_pack_fits(static_cast<int>(m)) ||
+        al % 16) {
+        set_err(err, PF_ERR_INVALID_PARAMETERS,
+                "dibit path needs e < m, 3 <= width <= 8, a record that fits a pack tile and "
+                "16-byte aligned record arrays");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceState& d = ctx->devs[0];
+    PF_CUDA(cudaSetDevice(d.device));
+    PF_CUDA(grow(d.d_scratch, d.scratch_words,
+                 sb::planes_scratch_words(static_cast<long long>(n), static_cast<int>(m))));
+    sb::FilterArgs a{};
+    a.text = d_text;
+    a.pattern = d_pattern;
+    a.dibits = true;
+    a.ntext = d_ntext;
+    a.npattern = d_npattern;
+    a.pitch = sb::dibit_pitch(static_cast<int>(m));
+    a.n = static_cast<long long>(n);
+    a.m = static_cast<int>(m);
+    a.e = e;
+    a.width = width;
+    a.accept = d_accept_bitmap;
+    a.estimates = d_estimates;
+    a.planes = d.d_scratch;
+    a.planes_words = d.scratch_words;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PF_CUDA(scratch_acquire(d, s));
+    PF_CUDA(sb::launch_filter(a, s));
+    PF_CUDA(scratch_release(d, s));
+    return PF_OK;
+}
+
 int pf_ctx_create(const int* devices, int count, pf_ctx** out) {
     if (!out) return PF_ERR_NULL_ARGUMENT;
     *out = nullptr;
@@ -671,6 +798,8 @@ void pf_ctx_destroy(pf_ctx* ctx) {
         for (int b = 0; b < 2; ++b) {
             if (d.h_nib[b]) cudaFreeHost(d.h_nib[b]);
             cudaFree(d.d_nib[b]);
+            if (d.h_nrow[b]) cudaFreeHost(d.h_nrow[b]);
+            cudaFree(d.d_nrow[b]);
             if (d.nib_ev[b]) cudaEventDestroy(d.nib_ev[b]);
             if (d.h_pk[b]) cudaFreeHost(d.h_pk[b]);
             cudaFree(d.d_pk[b]);

@@ -112,6 +112,92 @@ SB_AVX512 void pack_rows_avx512(const uint8_t* text, const uint8_t* pattern, siz
     if (_mm512_test_epi8_mask(acc, acc)) scan_bad(text, pattern, stride, m, lo, hi, bad);
 }
 
+// ---- dibit records (pack.cuh) ------------------------------------------------------
+// Per 64 columns: codes = (byte >> 1) & 3; within each 16-byte lane the four
+// dwords (columns q, q+4, q+8, q+12 at the same byte) are merged with
+// lane-local byte shifts and 2/4/6-bit dword shifts; the low dword of every
+// lane is the packed word (vpcompressd keeps those 4). N columns are recorded
+// in the returned 64-bit mask (bit 3 of the byte).
+SB_AVX512 inline __m128i dib64(__m512i v) {
+    const __m512i c = _mm512_and_si512(_mm512_srli_epi16(v, 1), _mm512_set1_epi8(0x03));
+    const __m512i c1 = _mm512_slli_epi32(_mm512_bsrli_epi128(c, 4), 2);
+    const __m512i c2 = _mm512_slli_epi32(_mm512_bsrli_epi128(c, 8), 4);
+    const __m512i c3 = _mm512_slli_epi32(_mm512_bsrli_epi128(c, 12), 6);
+    const __m512i r = _mm512_ternarylogic_epi32(_mm512_or_si512(c, c1), c2, c3, 0xFE);  // a|b|c
+    return _mm512_castsi512_si128(_mm512_maskz_compress_epi32(0x1111, r));
+}
+
+// Rows [lo, hi) -> dibit rows (and N-plane rows when nplanes != nullptr).
+// Returns true when any of these rows holds an N.
+SB_AVX512 bool pack_dibit_rows_avx512(const uint8_t* text, const uint8_t* pattern, size_t stride,
+                                      int m, long long lo, long long hi, uint8_t* out_text,
+                                      uint8_t* out_pattern, uint8_t* n_text, uint8_t* n_pattern,
+                                      HostBad* bad) {
+    const size_t dp = dibit_pitch(m), np = nplane_pitch(m);
+    alignas(64) uint8_t lb[64];
+    for (int i = 0; i < 64; ++i) lb[i] = static_cast<uint8_t>(i ^ 1);
+    for (uint8_t c : {'A', 'C', 'G', 'N', 'T'}) lb[c & 63] = c;
+    const __m512i lut = _mm512_load_si512(lb);
+    const __m512i bitn = _mm512_set1_epi8(0x08);
+    __m512i acc = _mm512_setzero_si512();
+    uint64_t anyn = 0;
+    auto mask_of = [](int w) -> __mmask64 {
+        return w >= 64 ? ~0ull : (w <= 0 ? 0ull : ((1ull << w) - 1));
+    };
+    for (long long r = lo; r < hi; ++r) {
+        for (int f = 0; f < 2; ++f) {
+            const uint8_t* s = (f == 0 ? text : pattern) + r * stride;
+            uint8_t* d = (f == 0 ? out_text : out_pattern) + r * dp;
+            uint8_t* nd = n_text ? (f == 0 ? n_text : n_pattern) + r * np : nullptr;
+            for (int c0 = 0; c0 < m; c0 += 64) {
+                const __mmask64 k = mask_of(m - c0);
+                const __m512i v = _mm512_maskz_loadu_epi8(k, s + c0);
+                acc = _mm512_ternarylogic_epi32(acc, _mm512_maskz_permutexvar_epi8(k, v, lut), v,
+                                                0xF6);  // acc | (lut(v) ^ v)
+                const uint64_t nm = _mm512_test_epi8_mask(v, bitn);
+                anyn |= nm;
+                const int ob = static_cast<int>(dp) - c0 / 4;  // bytes left in the row
+                _mm_mask_storeu_epi8(d + c0 / 4, static_cast<__mmask16>(ob >= 16 ? 0xFFFF : ((1u << ob) - 1)),
+                                     dib64(v));
+                if (nd) {
+                    const int nb = static_cast<int>(np) - c0 / 8;
+                    const __m128i nv = _mm_cvtsi64_si128(static_cast<long long>(nm));
+                    _mm_mask_storeu_epi8(nd + c0 / 8, static_cast<__mmask16>(nb >= 8 ? 0xFF : ((1u << nb) - 1)), nv);
+                }
+            }
+        }
+    }
+    if (_mm512_test_epi8_mask(acc, acc)) scan_bad(text, pattern, stride, m, lo, hi, bad);
+    return anyn != 0;
+}
+
+bool pack_dibit_rows_scalar(const uint8_t* text, const uint8_t* pattern, size_t stride, int m,
+                            long long lo, long long hi, uint8_t* out_text, uint8_t* out_pattern,
+                            uint8_t* n_text, uint8_t* n_pattern, HostBad* bad) {
+    const size_t dp = dibit_pitch(m), np = nplane_pitch(m);
+    bool ok = true, anyn = false;
+    for (long long r = lo; r < hi; ++r)
+        for (int f = 0; f < 2; ++f) {
+            const uint8_t* s = (f == 0 ? text : pattern) + r * stride;
+            uint8_t* d = (f == 0 ? out_text : out_pattern) + r * dp;
+            std::memset(d, 0, dp);
+            uint8_t* nd = n_text ? (f == 0 ? n_text : n_pattern) + r * np : nullptr;
+            if (nd) std::memset(nd, 0, np);
+            for (int c = 0; c < m; ++c) {
+                const uint8_t x = s[c];
+                ok &= valid_base(x);
+                const int w = c / 16, rem = c % 16, q = rem % 4, t = rem / 4;
+                d[4 * w + q] |= static_cast<uint8_t>(((x >> 1) & 3u) << (2 * t));
+                if ((x >> 3) & 1u) {
+                    anyn = true;
+                    if (nd) nd[c / 8] |= static_cast<uint8_t>(1u << (c % 8));
+                }
+            }
+        }
+    if (!ok) scan_bad(text, pattern, stride, m, lo, hi, bad);
+    return anyn;
+}
+
 bool has_avx512() {
     static const bool v = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
                           __builtin_cpu_supports("avx512vl") &&
@@ -266,6 +352,43 @@ void host_copy_parallel(void* dst, const void* src, size_t bytes) {
         body(0);
     else
         pool().run(tasks, body);
+}
+
+void host_pack_dibits_parallel(const uint8_t* text, const uint8_t* pattern, size_t stride,
+                               long long n, int m, uint8_t* out_text, uint8_t* out_pattern,
+                               uint8_t* n_text, uint8_t* n_pattern, HostBad* bad, bool* has_n,
+                               bool allow_simd) {
+    *has_n = false;
+    if (n <= 0) return;
+    const bool simd = allow_simd && has_avx512();
+    const unsigned nt = host_pack_threads();
+    const size_t tasks = static_cast<size_t>(std::max<long long>(
+        1, std::min<long long>((n + 1023) / 1024, 4ll * nt)));
+    std::vector<HostBad> bads(tasks);
+    std::vector<char> nflags(tasks, 0);
+    auto run = [&](uint8_t* nt_out, uint8_t* np_out) {
+        auto body = [&](size_t t) {
+            const long long lo = n * static_cast<long long>(t) / static_cast<long long>(tasks);
+            const long long hi = n * static_cast<long long>(t + 1) / static_cast<long long>(tasks);
+            const bool any = simd ? pack_dibit_rows_avx512(text, pattern, stride, m, lo, hi, out_text,
+                                                           out_pattern, nt_out, np_out, &bads[t])
+                                  : pack_dibit_rows_scalar(text, pattern, stride, m, lo, hi, out_text,
+                                                           out_pattern, nt_out, np_out, &bads[t]);
+            nflags[t] = any ? 1 : 0;
+        };
+        if (tasks == 1)
+            body(0);
+        else
+            pool().run(tasks, body);
+    };
+    // first pass: dibits, validation, N detection; the N planes are written
+    // (second pass) only when some row of the batch holds an N
+    run(nullptr, nullptr);
+    for (const auto& b : bads)
+        if (b.any) bad->offer(b.pair, b.field, b.pos, b.byte);
+    if (bad->any) return;
+    for (char f : nflags) *has_n = *has_n || f;
+    if (*has_n && n_text && n_pattern) run(n_text, n_pattern);
 }
 
 }  // namespace sb

@@ -38,6 +38,14 @@ void host_pack_nibbles_parallel(const uint8_t* text, const uint8_t* pattern, siz
                                 HostBad* bad, unsigned threads = 0, bool allow_simd = true);
 unsigned host_pack_threads();
 
+// All n pairs into dibit records (pack.cuh) on the worker pool. has_n reports
+// whether any base is 'N'; only then are the N-plane records (n_text,
+// n_pattern; nplane_pitch(m) bytes per record) written.
+void host_pack_dibits_parallel(const uint8_t* text, const uint8_t* pattern, size_t stride,
+                               long long n, int m, uint8_t* out_text, uint8_t* out_pattern,
+                               uint8_t* n_text, uint8_t* n_pattern, HostBad* bad, bool* has_n,
+                               bool allow_simd = true);
+
 // memcpy on the same worker pool (pageable -> pinned staging copies).
 void host_copy_parallel(void* dst, const void* src, size_t bytes);
 

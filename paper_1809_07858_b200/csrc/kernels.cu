@@ -274,6 +274,8 @@ cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
     if (a.planes == nullptr || a.planes_words < plane_words(a.n, a.m)) return cudaErrorInvalidValue;
     cudaError_t st =
         a.packed_text ? launch_pack_planes(a.packed_text, a.packed_pattern, a.n, a.m, a.planes, s)
+        : a.dibits    ? launch_pack_dibits(a.text, a.pattern, a.ntext, a.npattern, a.n, a.m,
+                                           a.planes, s)
         : a.nibbles   ? launch_pack_nibbles(a.text, a.pattern, a.n, a.m, a.planes, s)
                       : launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, a.planes, a.err_flag, s);
     if (st != cudaSuccess) return st;

@@ -44,6 +44,9 @@ struct FilterArgs {
     uint32_t* planes;      // device scratch for the pair-sliced planes (pack.cuh)
     size_t planes_words;   // available words in planes
     bool nibbles;          // text/pattern are host-packed nibble records (pitch unused)
+    bool dibits;           // text/pattern are dibit records (pack.cuh; pitch unused)
+    const uint8_t* ntext;     // dibits: N-plane records, or null when the batch has no N
+    const uint8_t* npattern;
     const uint64_t* packed_text;     // non-null: pre-packed planes input (pack_planes.cu);
     const uint64_t* packed_pattern;  //   text/pattern/pitch unused
 };
@@ -59,6 +62,11 @@ cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitc
 bool nibble_pack_fits(int m);
 cudaError_t launch_pack_nibbles(const uint8_t* text, const uint8_t* pattern, long long n, int m,
                                 uint32_t* planes, cudaStream_t s);
+// Stage 1 from dibit records (+ optional N-plane records; pack.cuh).
+bool dibit_pack_fits(int m);
+cudaError_t launch_pack_dibits(const uint8_t* text, const uint8_t* pattern, const uint8_t* ntext,
+                               const uint8_t* npattern, long long n, int m, uint32_t* planes,
+                               cudaStream_t s);
 // Stage 1 from packed_sequence planes ([n][3][ceil(m/64)] u64 per sequence).
 cudaError_t launch_pack_planes(const uint64_t* text, const uint64_t* pattern, long long n, int m,
                                uint32_t* planes, cudaStream_t s);

@@ -53,4 +53,13 @@ __host__ __device__ inline size_t plane_index(int s, long long g, int col, int k
 // column. Validation happens on the host, which packs.
 __host__ __device__ inline size_t nibble_pitch(int m) { return 4 * static_cast<size_t>((m + 7) / 8); }
 
+// Dibit records: the compact upload format (host_pack.cpp). A record of m
+// columns is ceil(m/16) little-endian uint32 words; byte q of word w holds the
+// 2-bit codes (ASCII bits 1-2: lo, hi) of columns 16w+q, 16w+q+4, 16w+q+8 and
+// 16w+q+12 at bits 0-1, 2-3, 4-5, 6-7; columns >= m are zero. N is carried
+// separately: N-plane records of ceil(m/32) uint32 words (bit c = column c is
+// 'N'), sent only for chunks that contain an N.
+__host__ __device__ inline size_t dibit_pitch(int m) { return 4 * static_cast<size_t>((m + 15) / 16); }
+__host__ __device__ inline size_t nplane_pitch(int m) { return 4 * static_cast<size_t>((m + 31) / 32); }
+
 }  // namespace sb

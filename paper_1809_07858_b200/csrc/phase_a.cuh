@@ -210,6 +210,77 @@ __device__ __forceinline__ void gather_chunk_nib(const uint8_t* __restrict__ seq
         }
 }
 
+// gather_chunk for dibit records (pack.cuh dibit format, validated by the
+// host): a 16-column chunk is one word per row; column 4t+q of the chunk sits
+// in byte q at bits 2t (lo) and 2t+1 (hi), so plane k of column group t
+// reaches bit 8q+i of the accumulator by one shift. The N plane comes from the
+// optional N-plane rows (bit c = column c); without them every column is
+// N-free.
+template <bool EDGE, int NCG, bool HAS_N>
+__device__ __forceinline__ void gather_chunk_dib(const uint8_t* __restrict__ seq, size_t pitch,
+                                                 const uint8_t* __restrict__ nseq, size_t npitch,
+                                                 int col0, int m, uint32_t* __restrict__ dst,
+                                                 int dstride) {
+    uint32_t O[NCG][3][4];
+#pragma unroll
+    for (int cg = 0; cg < NCG; ++cg)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) O[cg][k][q] = 0u;
+#pragma unroll 1
+    for (int g8 = 0; g8 < 4; ++g8) {
+        uint32_t v[8], nv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            v[i] = *reinterpret_cast<const uint32_t*>(seq + (8 * g8 + i) * pitch + col0 / 4);
+            if constexpr (HAS_N) {
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(
+                    nseq + (8 * g8 + i) * npitch + (col0 / 32) * 4);
+                nv[i] = w >> (col0 & 31);  // the chunk's 16 N bits at bits 0..15
+            }
+        }
+        uint32_t acc[3][NCG];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int cg = 0; cg < NCG; ++cg) acc[k][cg] = 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int cg = 0; cg < NCG; ++cg) {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const int s = i - (2 * cg + k);
+                    const uint32_t u =
+                        s >= 0 ? v[i] * (1u << s) : __umulhi(v[i], 1u << (32 + s));
+                    acc[k][cg] |= u & (0x01010101u << i);
+                }
+                if constexpr (HAS_N) {
+                    // bits 4cg..4cg+3 of the N word -> bit 8q (x * (1 + 2^7 + 2^14 + 2^21)) -> 8q+i
+                    const uint32_t x = (nv[i] >> (4 * cg)) & 0xFu;
+                    acc[2][cg] |= ((x * 0x00204081u) & 0x01010101u) << i;
+                }
+            }
+#pragma unroll
+        for (int cg = 0; cg < NCG; ++cg)
+#pragma unroll
+            for (int k = 0; k < (HAS_N ? 3 : 2); ++k)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    O[cg][k][q] = __byte_perm(O[cg][k][q], acc[k][cg], 0x0321 | ((4 + q) << 12));
+    }
+#pragma unroll
+    for (int cg = 0; cg < NCG; ++cg)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int col = 4 * cg + q;
+            if (EDGE && col0 + col >= m) continue;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) dst[(col * 3 + k) * dstride] = O[cg][k][q];
+        }
+}
+
 // A chunk entirely outside [0, m): every column is N.
 __device__ __forceinline__ void fill_oob_chunk(uint32_t* __restrict__ dst, int dstride) {
 #pragma unroll

@@ -1,10 +1,11 @@
-"""GPU parity of the host-pack upload path: records packed into nibble records
-on the host's cores (csrc/host_pack.cpp), filtered on the device from nibbles
-(pack.cuh nibble format, phase_a.cuh gather_chunk_nib) — against the oracle.
+"""GPU parity of the host-pack upload path: records packed on the host's cores
+(csrc/host_pack.cpp) into dibit records (+ N planes when a chunk has an N; the
+default) or nibble records, filtered on the device from them (pack.cuh formats,
+phase_a.cuh gather_chunk_dib / gather_chunk_nib) — against the oracle.
 
 pf_shouji_filter_batch routes host batches of >= 65536 pairs through this path
 (PF_HOST_PACK unset), so the large-batch tests below exercise it end to end,
-including chunk boundaries (512Ki pairs per chunk) and error order across chunks.
+including chunk boundaries (256Ki pairs per chunk) and error order across chunks.
 """
 import numpy as np
 import pytest
@@ -78,7 +79,7 @@ def test_nibble_device_path_rejects_bad_parameters(gpu):
 
 
 @pytest.mark.parametrize("n", [65536, 65536 + 31, 1_200_001])
-def test_host_batch_uses_nibbles_and_matches(gpu, oracle, n):
+def test_host_batch_uses_dibits_and_matches(gpu, oracle, n):
     rng = np.random.default_rng(n)
     t, p = mutated(rng, n, 100, alphabet=ACGT)
     before = gpu.launch_count()
@@ -86,7 +87,7 @@ def test_host_batch_uses_nibbles_and_matches(gpu, oracle, n):
     a1, e1, _ = gpu.shouji_filter_batch(t, p, 5, estimates=True)
     assert gpu.launch_count() > before
     h1, _ = gpu.transfer_bytes()
-    assert h1 - h0 == 2 * n * gpu.nibble_pitch(100)  # nibble records crossed PCIe, not ASCII
+    assert h1 - h0 == 2 * n * gpu.dibit_pitch(100)  # dibit records (no N) crossed PCIe, not ASCII
     a2, e2, _ = oracle.shouji_batch(t, p, 5)
     assert (a1 == a2).all() and (e1 == e2).all()
 
@@ -142,3 +143,47 @@ def test_host_pack_with_device_shards(gpu, oracle):
         assert (ei.value.pair, ei.value.field, ei.value.position()) == (250_000, 0, 2)
     finally:
         ctx.close()
+
+
+def run_dibits(gpu, t, p, e, width=4):
+    import torch
+    n, m = t.shape
+    dt, dq, nt, nq = gpu.host_pack_dibits(t, p)
+    tens = [torch.from_numpy(a).cuda() if a is not None else None for a in (dt, dq, nt, nq)]
+    acc = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    est = torch.zeros(n, dtype=torch.int32, device="cuda")
+    gpu.shouji_filter_dibits_device(tens[0].data_ptr(), tens[1].data_ptr(), n, m, e, acc.data_ptr(),
+                                    d_ntext=tens[2].data_ptr() if nt is not None else None,
+                                    d_npattern=tens[3].data_ptr() if nq is not None else None,
+                                    width=width, d_estimates=est.data_ptr())
+    torch.cuda.synchronize()
+    return acc.cpu().numpy().view(np.uint32), est.cpu().numpy().view(np.uint32), nt is not None
+
+
+@pytest.mark.parametrize("m", [1, 2, 5, 15, 16, 17, 31, 33, 64, 100, 127, 128, 150, 250, 256, 300])
+@pytest.mark.parametrize("alphabet", ["ACGT", "ACGTN"])
+def test_dibit_device_path(gpu, oracle, m, alphabet):
+    rng = np.random.default_rng(m + len(alphabet))
+    a = np.frombuffer(alphabet.encode(), np.uint8)
+    t, p = mutated(rng, 1500 + 3 * m, m, alphabet=a)
+    for e in sorted({0, min(m - 1, 2), min(m - 1, 5), min(m - 1, 17), m - 1}):
+        a1, e1, had_n = run_dibits(gpu, t, p, e)
+        assert had_n == (alphabet == "ACGTN")
+        a2, e2, _ = oracle.shouji_batch(t, p, e)
+        assert (a1 == a2).all() and (e1 == e2).all(), (m, e, alphabet)
+
+
+def test_host_batch_chunks_with_and_without_n(gpu, oracle):
+    """Chunks without N upload dibits only; a chunk with one N adds its N planes."""
+    rng = np.random.default_rng(17)
+    n = 700_000
+    t, p = mutated(rng, n, 100, alphabet=ACGT)
+    t[400_000, 50] = ord("N")  # second chunk only
+    h0, _ = gpu.transfer_bytes()
+    a1, e1, _ = gpu.shouji_filter_batch(t, p, 5, estimates=True)
+    h1, _ = gpu.transfer_bytes()
+    a2, e2, _ = oracle.shouji_batch(t, p, 5)
+    assert (a1 == a2).all() and (e1 == e2).all()
+    chunk = 1 << 18
+    cn = min(chunk, n - chunk)
+    assert h1 - h0 == 2 * n * gpu.dibit_pitch(100) + 2 * cn * gpu.nplane_pitch(100)

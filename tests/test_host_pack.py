@@ -161,3 +161,80 @@ def test_host_pack_output_alignment(offset):
     assert (raw_p[base_p:base_p + n * np_].reshape(n, np_) == ref_nibbles(p)).all()
     assert (raw_t[:base_t] == 0xEE).all() and (raw_t[base_t + n * np_:] == 0xEE).all()
     assert (raw_p[:base_p] == 0xEE).all() and (raw_p[base_p + n * np_:] == 0xEE).all()
+
+
+# ---- dibit records (the default upload format) ---------------------------------------
+
+def ref_dibits(arr):
+    """byte q of word w = codes of columns 16w+q, +4, +8, +12 at bits 0-1, 2-3, 4-5, 6-7;
+    code = ASCII bits 1-2. N planes: bit c = column c is 'N' (LSB-first u32 words)."""
+    n, m = arr.shape
+    words = (m + 15) // 16
+    pad = np.zeros((n, words * 16), np.uint8)
+    pad[:, :m] = arr
+    code = (pad >> 1) & 3
+    blk = code.reshape(n, words, 4, 4)  # [word][t][q] -> column 16w + 4t + q
+    out = np.zeros((n, words, 4), np.uint8)
+    for t in range(4):
+        out |= (blk[:, :, t, :] << (2 * t)).astype(np.uint8)
+    nb = np.zeros((n, ((m + 31) // 32) * 32), np.uint8)
+    nb[:, :m] = arr == ord("N")
+    nplanes = np.packbits(nb, axis=1, bitorder="little")
+    return out.reshape(n, words * 4), nplanes
+
+
+def host_pack_dib(t, p, simd):
+    n, m = t.shape
+    dp, npitch = L.lib.pf_dibit_pitch(m), L.lib.pf_nplane_pitch(m)
+    bufs = [np.full((n, w), 0xEE, np.uint8) for w in (dp, dp, npitch, npitch)]
+    has_n = C.c_int(-1)
+    err = L.PfError()
+    st = L.lib.pf_host_pack_dibits(t.ctypes.data_as(C.c_void_p), p.ctypes.data_as(C.c_void_p), m,
+                                   n, m, *[b.ctypes.data_as(C.c_void_p) for b in bufs],
+                                   C.byref(has_n), simd, C.byref(err))
+    return st, bufs, has_n.value, err
+
+
+def test_dibit_pitches():
+    for m, dp, npitch in [(1, 4, 4), (16, 4, 4), (17, 8, 4), (100, 28, 16), (150, 40, 20),
+                          (250, 64, 32), (256, 64, 32)]:
+        assert (L.lib.pf_dibit_pitch(m), L.lib.pf_nplane_pitch(m)) == (dp, npitch)
+
+
+@pytest.mark.parametrize("simd", [1, 0])
+@pytest.mark.parametrize("n,m,alphabet", [(1, 1, b"ACGT"), (33, 15, b"ACGT"), (300, 16, b"ACGTN"),
+                                          (777, 100, b"ACGT"), (777, 100, b"ACGTN"),
+                                          (513, 127, b"ACGTN"), (200, 129, b"ACGT"),
+                                          (129, 250, b"ACGTN"), (5000, 100, b"ACGT")])
+def test_host_pack_dibits_matches_format(simd, n, m, alphabet):
+    rng = np.random.default_rng(n + m)
+    t, p = rand_records(rng, n, m, alphabet), rand_records(rng, n, m, alphabet)
+    st, (dt, dq, nt, nq), has_n, _ = host_pack_dib(t, p, simd)
+    assert st == 0
+    rt, rnt = ref_dibits(t)
+    rp, rnp = ref_dibits(p)
+    assert (dt == rt).all() and (dq == rp).all()
+    assert has_n == int(bool((t == ord("N")).any() or (p == ord("N")).any()))
+    if has_n:
+        assert (nt == rnt).all() and (nq == rnp).all()
+    else:
+        assert (nt == 0xEE).all() and (nq == 0xEE).all()  # not written without an N
+
+
+@pytest.mark.parametrize("simd", [1, 0])
+def test_host_pack_dibits_first_illegal_byte(simd):
+    rng = np.random.default_rng(5)
+    n, m = 7000, 100
+    t = rand_records(rng, n, m, b"ACGT")
+    p = t.copy()
+    p[6000, 3] = ord("x")
+    t[6000, 70] = ord("a")
+    p[100, 98] = ord("U")
+    st, _, _, err = host_pack_dib(t, p, simd)
+    assert st == L.PF_ERR_ILLEGAL_CHARACTER
+    assert (err.pair, err.field, err.position, err.byte) == (100, 1, 98, ord("U"))
+    for b in (0x00, 0xC1, 0x4E | 0x80, ord("n")):
+        q = t.copy()
+        q[42, 17] = b
+        st, _, _, err = host_pack_dib(q, t.copy(), simd)
+        assert st == L.PF_ERR_ILLEGAL_CHARACTER and (err.pair, err.field, err.position) == (42, 0, 17)
