@@ -340,6 +340,15 @@ def run_ours(args, rank, world, local_rank):
     a_gpu = accept[: chk // 32].cpu().numpy().view(np.uint32)
     assert (a_gpu == a_ref).all(), "benchmarked kernel disagrees with the oracle"
 
+    # per-stage split of the same step (outside the timed region): pack vs search, CUDA
+    # events recorded between the two launches on the library's stream
+    stage_ms = None
+    try:
+        stage_ms = pf.profile_stages(text.data_ptr(), pattern.data_ptr(), pitch, n, m, e,
+                                     accept.data_ptr(), errflag.data_ptr(), reps=3, ctx=ctx)
+    except Exception:
+        stage_ms = None
+
     # ---- e2e: public host API from pinned host records ----------------------------------
     e2e = None
     t_e2e = (t_wall1, t_wall1)
@@ -407,6 +416,22 @@ def run_ours(args, rank, world, local_rank):
                            "sb::shouji_search_w4<5> (map+search+commit+accept); achieved is over "
                            "the whole step (both launches)",
                 "kernel_ms_avg": kern_avg_ms}
+    if stage_ms is not None:
+        pk_ms, se_ms = stage_ms
+        pack_bytes = n * (2 * m + 2 * 3 * m * 4 / 32)  # ASCII in, 3 planes x 2 sequences out
+        # algorithmic LOP3 of the search per 32-pair group and window: map 3 + key 5 per
+        # diagonal, compare 4 + mux 7 per diagonal after the first, commit FSM + tally 17
+        windows = ((m + 3 + 3) // 4) * 4
+        lop3_pair = ((2 * e + 1) * 8 + 2 * e * 11 + 17) * windows / 32
+        roofline["per_kernel"] = [
+            {"kernel": "sb::pack_tile_kernel<8,4,0>", "ms": pk_ms, "share": pk_ms / (pk_ms + se_ms),
+             "bound": "hbm", "algorithmic_bytes_per_pair": pack_bytes / n,
+             "achieved": pack_bytes / (pk_ms * 1e-3) / 1e9, "unit": "GB/s",
+             "frac": pack_bytes / (pk_ms * 1e-3) / 1e9 / float(peaks["hbm_gbs"])},
+            {"kernel": f"sb::shouji_search_w4<{e}>", "ms": se_ms, "share": se_ms / (pk_ms + se_ms),
+             "bound": "int (ALU pipe, LOP3)", "algorithmic_lop3_per_pair": lop3_pair,
+             "achieved": lop3_pair * n / (se_ms * 1e-3), "unit": "lane-ops/s"},
+        ]
     int_view = None
     if rank == 0:
         try:
@@ -414,6 +439,10 @@ def run_ours(args, rank, world, local_rank):
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
             ops_pair = 25 * (2 * e + 1) * ((m + 31) // 32) + 8 * m  # BASELINE.md OPS(m,E)
             int_bound = lop3 / ops_pair
+            if "per_kernel" in roofline:
+                sk = roofline["per_kernel"][1]
+                sk["peak"] = lop3
+                sk["frac"] = sk["achieved"] / lop3
             int_view = {"ops_per_pair_formula": ops_pair, "lop3_lane_ops_per_s": lop3,
                         "lop3_lanes_per_clk_per_sm_at_max_clock":
                             lop3 / (sms * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6),

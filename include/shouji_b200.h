@@ -124,6 +124,14 @@ int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint
                                   uint32_t* d_accept_bitmap, uint32_t* d_estimates,
                                   uint32_t* d_err_flag, void* stream);
 
+/* Diagnostic: pf_shouji_filter_device_async's two stages timed separately
+ * with CUDA events on the context's stream (pack = records -> planes, search =
+ * map + select + commit + accept), averaged over reps synchronous runs. */
+int pf_shouji_profile_stages(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                             size_t pitch, size_t n, uint32_t m, uint32_t e, uint32_t width,
+                             uint32_t* d_accept_bitmap, uint32_t* d_err_flag, int reps,
+                             float* pack_ms, float* search_ms);
+
 /* Measured integer pipe throughput on the ctx's first device (diagnostic for
  * the INT roofline): op 0 = LOP3, 1 = funnel shift, 2 = PRMT, 3 = IMAD.
  * Writes lane-operations per second. */

@@ -35,6 +35,7 @@ from .api import (  # noqa: F401
     shouji_filter_device,
     shouji_filter_device_async,
     int_peak,
+    profile_stages,
     packed_words,
     pack_planes,
     shouji_filter_packed_batch,

@@ -37,7 +37,7 @@ EXPORTED = [
     "pf_dataset_source", "pf_dataset_write_tsv", "pf_dataset_free", "pf_banded_edit_distance_batch",
     "pf_nibble_pitch", "pf_host_pack_nibbles", "pf_shouji_filter_nibbles_device",
     "pf_transfer_bytes", "pf_dibit_pitch", "pf_nplane_pitch", "pf_host_pack_dibits",
-    "pf_shouji_filter_dibits_device", "pf_magnet_filter_batch", "pf_magnet_filter_device",
+    "pf_shouji_filter_dibits_device", "pf_shouji_profile_stages", "pf_magnet_filter_batch", "pf_magnet_filter_device",
     "pf_magnet_filter_one", "pf_packed_words", "pf_shouji_filter_packed_batch",
     "pf_shouji_filter_packed_device",
 ]
@@ -102,6 +102,9 @@ def _bind(lib):
                                                     C.POINTER(PfError)]),
         "pf_nibble_pitch": (_sz, [_u32]),
         "pf_dibit_pitch": (_sz, [_u32]),
+        "pf_shouji_profile_stages": (C.c_int, [_vp, _vp, _vp, _sz, _sz, _u32, _u32, _u32, _vp, _vp,
+                                               C.c_int, C.POINTER(C.c_float),
+                                               C.POINTER(C.c_float)]),
         "pf_nplane_pitch": (_sz, [_u32]),
         "pf_host_pack_dibits": (C.c_int, [_vp, _vp, _sz, _sz, _u32, _vp, _vp, _vp, _vp,
                                           C.POINTER(C.c_int), C.c_int, C.POINTER(PfError)]),

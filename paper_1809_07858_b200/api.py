@@ -576,6 +576,18 @@ def shouji_filter_nibbles_device(d_text: int, d_pattern: int, n: int, m: int, e:
     _raise(st, err)
 
 
+def profile_stages(d_text: int, d_pattern: int, pitch: int, n: int, m: int, e: int, d_accept: int,
+                   d_err_flag: int, width: int = default_window_width, reps: int = 3,
+                   ctx: Context | None = None) -> tuple[float, float]:
+    """(pack ms, search ms) of the device path, timed per stage with CUDA events."""
+    ctx = ctx or default_context()
+    pk, se = C.c_float(), C.c_float()
+    _raise(L.lib.pf_shouji_profile_stages(ctx.handle, d_text, d_pattern, pitch, n, m, int(e),
+                                          int(width), d_accept, d_err_flag, int(reps), C.byref(pk),
+                                          C.byref(se)))
+    return float(pk.value), float(se.value)
+
+
 def int_peak(op: str = "lop3", ctx: Context | None = None) -> float:
     """Measured integer lane-ops/s of one instruction class on the ctx's device."""
     ctx = ctx or default_context()

@@ -1282,6 +1282,49 @@ int pf_shouji_filter_device_async(pf_ctx* ctx, const uint8_t* d_text, const uint
     return PF_OK;
 }
 
+int pf_shouji_profile_stages(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
+                             size_t pitch, size_t n, uint32_t m, uint32_t e, uint32_t width,
+                             uint32_t* d_accept_bitmap, uint32_t* d_err_flag, int reps,
+                             float* pack_ms, float* search_ms) {
+    pf_error* err = nullptr;
+    if (!ctx || !d_err_flag || !pack_ms || !search_ms || reps < 1) return PF_ERR_NULL_ARGUMENT;
+    if (n == 0 || !d_text || !d_pattern || !d_accept_bitmap) return PF_ERR_NULL_ARGUMENT;
+    if (m == 0 || e >= m || width < 3 || width > 8 || pitch % 4 != 0 || pitch < m)
+        return PF_ERR_INVALID_PARAMETERS;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceState& d = ctx->devs[0];
+    PF_CUDA(cudaSetDevice(d.device));
+    cudaEvent_t ev[3];
+    for (auto& x : ev) PF_CUDA(cudaEventCreate(&x));
+    sb::FilterArgs a{};
+    a.text = d_text;
+    a.pattern = d_pattern;
+    a.pitch = pitch;
+    a.n = static_cast<long long>(n);
+    a.m = static_cast<int>(m);
+    a.e = e;
+    a.width = width;
+    a.accept = d_accept_bitmap;
+    a.err_flag = d_err_flag;
+    a.stage_event = ev[1];
+    double pk = 0.0, se = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        PF_CUDA(cudaEventRecord(ev[0], d.stream));
+        PF_CUDA(launch_any(d, a, d.stream));
+        PF_CUDA(cudaEventRecord(ev[2], d.stream));
+        PF_CUDA(cudaEventSynchronize(ev[2]));
+        float t0 = 0.f, t1 = 0.f;
+        PF_CUDA(cudaEventElapsedTime(&t0, ev[0], ev[1]));
+        PF_CUDA(cudaEventElapsedTime(&t1, ev[1], ev[2]));
+        pk += t0;
+        se += t1;
+    }
+    for (auto& x : ev) cudaEventDestroy(x);
+    *pack_ms = static_cast<float>(pk / reps);
+    *search_ms = static_cast<float>(se / reps);
+    return PF_OK;
+}
+
 int pf_int_peak(pf_ctx* ctx, int op, double* ops_per_second) {
     pf_error* err = nullptr;
     if (!ctx || !ops_per_second) return PF_ERR_NULL_ARGUMENT;

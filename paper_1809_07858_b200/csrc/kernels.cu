@@ -279,6 +279,10 @@ cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
         : a.nibbles   ? launch_pack_nibbles(a.text, a.pattern, a.n, a.m, a.planes, s)
                       : launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, a.planes, a.err_flag, s);
     if (st != cudaSuccess) return st;
+    if (a.stage_event != nullptr) {
+        st = cudaEventRecord(a.stage_event, s);
+        if (st != cudaSuccess) return st;
+    }
     if (use_fused(a.width, a.e, a.m)) return kSearchTable[a.e](a, s);
     return a.m <= 255 ? launch_generic<8>(a, s) : launch_generic<24>(a, s);
 }

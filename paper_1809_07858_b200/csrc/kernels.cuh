@@ -47,6 +47,7 @@ struct FilterArgs {
     bool dibits;           // text/pattern are dibit records (pack.cuh; pitch unused)
     const uint8_t* ntext;     // dibits: N-plane records, or null when the batch has no N
     const uint8_t* npattern;
+    cudaEvent_t stage_event;   // non-null: recorded between the pack and the search kernel
     const uint64_t* packed_text;     // non-null: pre-packed planes input (pack_planes.cu);
     const uint64_t* packed_pattern;  //   text/pattern/pitch unused
 };
