@@ -428,3 +428,20 @@ def test_device_calls_on_two_streams_share_scratch_safely(gpu):
     torch.cuda.synchronize()
     for (_, _, _, ref), acc in zip(data, outs):
         assert torch.equal(acc, ref)
+
+
+def test_profile_stages(gpu):
+    import torch
+    n, m, e = 1_000_000, 100, 5
+    pitch = gpu.device_pitch(m)
+    tt = torch.empty((n, pitch), dtype=torch.uint8, device="cuda")
+    pt = torch.empty((n, pitch), dtype=torch.uint8, device="cuda")
+    gpu.generate_device(1, 3, e, tt.data_ptr(), pt.data_ptr(), pitch, n, m)
+    acc = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pk, se = gpu.profile_stages(tt.data_ptr(), pt.data_ptr(), pitch, n, m, e, acc.data_ptr(),
+                                flag.data_ptr(), reps=2)
+    assert 0 < pk < 100 and 0 < se < 100
+    ref = torch.zeros_like(acc)
+    gpu.shouji_filter_device(tt.data_ptr(), pt.data_ptr(), pitch, n, m, e, ref.data_ptr())
+    assert torch.equal(acc, ref)
