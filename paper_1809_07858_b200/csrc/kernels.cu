@@ -13,18 +13,22 @@
 // over columns becomes an 8-state machine (Appendix B2 of SURVEY.md) applied
 // to 32 pairs per instruction.
 //
-//   phase A  (gather_chunk): 16 ASCII columns x 32 pairs are loaded with
-//            128-bit loads and bit-transposed in registers (funnel-rotate +
-//            LOP3 gather, then a PRMT 4x4 byte transpose) into per-column
-//            plane words lo/hi/N (ASCII bits 1/2/3), validating every byte on
-//            the way. Planes go to a thread-private shared-memory ring.
-//   phase B  (search + commit): per block of 4 windows, the 2E+1 diagonals
-//            are scanned in reference order with the strict-first-argmax key
-//            2*ones + bit0 (equivalent to shouji.cpp:26-28);
-//            the chosen slices drive the commit FSM and a bit-sliced counter.
+//   stage 1 (pack.cu, pack_planes.cu): records -> planes[seq][pair block][col]
+//            [plane][8 groups] in global memory. ASCII records arrive by TMA
+//            bulk copy into shared memory and are bit-transposed in registers
+//            (phase_a.cuh gather_chunk: FMA-pipe shifts, masked ORs, PRMT byte
+//            insertion), validating every byte; host-packed dibit / nibble
+//            records and packed_sequence planes have their own gathers.
+//   stage 2 (fused.cuh for width 4 and E <= 31; shouji_generic below for
+//            other widths, larger E and m > 255): per block of 4 windows the
+//            2E+1 diagonals are scanned in reference order with the strict
+//            first-argmin key 2*ones + bit0 (equivalent to shouji.cpp:26-28,
+//            SURVEY App. B1); the chosen slices drive the commit FSM and a
+//            bit-sliced counter; accept bits and estimates are written per group.
 //
-// Everything a thread touches in shared memory is private to it, so the
-// kernel has no barriers.
+// This unit holds the generic search, the small helper kernels (illegal-byte
+// locator, tally-bit transpose, e >= m short-circuit, repitch) and the launch
+// dispatch.
 #include <cuda_runtime.h>
 
 #include <atomic>
