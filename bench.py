@@ -11,12 +11,14 @@ DESIGN.md "Measurement"):
   stream, max over ranks, summed over ranks (weak scaling: every rank owns its
   own 30M pairs; no collective touches the data path).
 * e2e    — the same workload through the public host API
-  (pf_shouji_filter_batch) from pinned host records: H2D of every record,
-  kernel, D2H of the accept bitmap, every step (wall clock, max over ranks).
-* roofline — the fused kernel's algorithmic bytes (2m ASCII + 1/8 accept bit per
-  pair) over its average launch time, against MEASURED_PEAKS.json hbm_gbs; the
-  INT view (BASELINE.md formula and the measured LOP3 lane rate) is reported
-  beside it.
+  (pf_shouji_filter_batch) from pinned host ASCII records: the host cores pack
+  2-bit records chunk by chunk, H2D, kernels, D2H of the accept bitmap, every
+  step (wall clock, max over ranks); the H2D/D2H bytes are the library's count.
+* roofline — the step's algorithmic bytes (2m ASCII + 1/8 accept bit per
+  pair) over its average launch time, against MEASURED_PEAKS.json hbm_gbs;
+  per_kernel splits the step live (pack vs search, CUDA events between the two
+  launches) into the pack's HBM fraction and the search's fraction of the
+  measured LOP3 lane rate; the BASELINE.md INT formula view is beside it.
 * cpu_baseline — the unmodified reference library (oracle/_ref) on this host's
   cores over a bounded sample of the same records (rank 0, N=1 only).
 

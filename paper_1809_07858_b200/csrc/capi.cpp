@@ -399,7 +399,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     }
 
     // ---- host -> device ----------------------------------------------------
-    // Records land in the device layout (pitch = round16(m)). A caller buffer
+    // Records land in the device layout (pitch = round4(m)). A caller buffer
     // already in that layout is one DMA per sequence; otherwise rows are
     // streamed in chunks: contiguous DMA of the caller's rows into a device
     // staging slot, then a repitch kernel. Pageable input first goes through a

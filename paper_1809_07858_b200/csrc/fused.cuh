@@ -89,8 +89,8 @@ struct SearchCfg {
 // Column loads relative to a per-block base pointer: word (x*3 + k) * 8 of the
 // group's planes, x counted from the block's first column `col0`. CHECK: the
 // block touches columns outside [0, m), which read as N.
-// NC: planes are read-only for the kernel (separate pack kernel) and may use
-// the non-coherent path; the fused kernel writes them itself and must not.
+// NC: the planes are read-only while the search kernel runs (the pack kernel
+// wrote them in an earlier launch), so the non-coherent path may serve them.
 template <bool CHECK, bool NC = true>
 __device__ __forceinline__ void load_rel(const uint32_t* __restrict__ base, int x, int col0, int m,
                                          uint32_t (&v)[3]) {

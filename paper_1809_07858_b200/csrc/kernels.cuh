@@ -82,7 +82,7 @@ cudaError_t launch_locate(const uint8_t* text, const uint8_t* pattern, size_t pi
 cudaError_t launch_bits_transpose(const uint32_t* outplanes, long long n, int m, uint64_t* bits,
                                   cudaStream_t s);
 // Copy n rows of m bytes from a device buffer with any row stride into the
-// 16-byte-pitched layout the filter kernels read.
+// tight round4(m)-pitched layout the filter kernels read.
 cudaError_t launch_repitch(const uint8_t* src, size_t src_stride, uint8_t* dst, size_t dst_pitch,
                            long long n, int m, cudaStream_t s);
 // Exact Levenshtein distance per pair (Myers bit-vector); out[i] = d <= e ? d : -1.

@@ -1,4 +1,4 @@
-// Tile machinery shared by the pack kernel and the fused kernel: TMA bulk
+// Tile machinery of the pack kernels: TMA bulk
 // copies of 32-record groups into bank-skewed shared memory, completion on an
 // mbarrier, then the in-register gather of phase_a.cuh.
 #pragma once
