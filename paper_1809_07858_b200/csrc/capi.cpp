@@ -4,9 +4,11 @@
 // (proj/src/shouji.cpp:44-49, packed_sequence.cpp:8,27-28), device buffer and
 // pinned-staging management, the 32-pair-aligned static split across devices
 // (the contiguous chunking of parallel_for_pairs, proj/src/evaluate.cpp:36-37)
-// and the gather of per-device bitmaps. No compute happens here: every pair
-// goes through the sm_100a kernels in kernels.cu; without a device the calls
-// fail with PF_ERR_NO_DEVICE.
+// and the gather of per-device bitmaps. Every filter decision is computed by
+// the sm_100a kernels; the only host-side processing is the host-pack upload
+// stage (host_pack.cpp: records packed to 2-bit form and validated on the CPU
+// cores before they cross PCIe). Without a device the calls fail with
+// PF_ERR_NO_DEVICE.
 #include <cuda_runtime.h>
 
 #include <algorithm>
