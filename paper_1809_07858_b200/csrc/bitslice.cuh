@@ -17,6 +17,16 @@ __device__ __forceinline__ uint32_t rotr(uint32_t x, int s) {
     return __funnelshift_r(x, x, static_cast<unsigned>(s) & 31u);
 }
 
+// One LOP3 with an explicit truth table (imm = f(0xF0, 0xCC, 0xAA)). The asm
+// is opaque to the optimizer, so a hand-counted expression stays that count
+// (nvcc otherwise re-associates the compare/select chains into more LOP3s).
+template <unsigned IMM>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(IMM));
+    return d;
+}
+
 // Running "a < b" across planes 0..N-1 (LSB first): one LOP3 per plane.
 template <int NA, int NB>
 __device__ __forceinline__ uint32_t bs_less(const uint32_t (&a)[NA], const uint32_t (&b)[NB]) {
@@ -26,9 +36,14 @@ __device__ __forceinline__ uint32_t bs_less(const uint32_t (&a)[NA], const uint3
     for (int i = 0; i < N; ++i) {
         const uint32_t ai = i < NA ? a[i] : 0u;
         const uint32_t bi = i < NB ? b[i] : 0u;
-        lt = (~ai & bi) | (~(ai ^ bi) & lt);
+        lt = lop3<0x8E>(ai, bi, lt);  // (~ai & bi) | (~(ai ^ bi) & lt)
     }
     return lt;
+}
+
+// sel ? x : y, one LOP3.
+__device__ __forceinline__ uint32_t bs_select(uint32_t x, uint32_t y, uint32_t sel) {
+    return lop3<0xE4>(x, y, sel);
 }
 
 // counter += v (bit-sliced), truncating at NC planes.

@@ -54,12 +54,18 @@ __device__ __forceinline__ void make_cand4(uint32_t a, uint32_t b, uint32_t c, u
     out.s[2] = d;
 }
 
+// best = c if key(c) < key(best): 4 LOP3 for the strict compare (LSB first:
+// lt = ~c&b | ~(c^b)&lt, table 0x8E) and 7 for the select (lt ? c : best,
+// table 0xE4) — 11 per candidate, pinned with explicit lop3.
 __device__ __forceinline__ void update_best4(const Cand4& c, Cand4& best) {
-    const uint32_t lt = bs_less(c.k, best.k);
+    uint32_t lt = lop3<0x8E>(c.k[0], best.k[0], 0u);
+    lt = lop3<0x8E>(c.k[1], best.k[1], lt);
+    lt = lop3<0x8E>(c.k[2], best.k[2], lt);
+    lt = lop3<0x8E>(c.k[3], best.k[3], lt);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) best.k[i] = (c.k[i] & lt) | (best.k[i] & ~lt);
+    for (int i = 0; i < 4; ++i) best.k[i] = lop3<0xE4>(c.k[i], best.k[i], lt);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) best.s[i] = (c.s[i] & lt) | (best.s[i] & ~lt);
+    for (int i = 0; i < 3; ++i) best.s[i] = lop3<0xE4>(c.s[i], best.s[i], lt);
 }
 
 // commit_window as a state machine over S = tally bits (j, j+1, j+2).

@@ -127,9 +127,9 @@ shouji_generic(const uint32_t* __restrict__ planes, long long n, int m, int e,
             } else {
                 const uint32_t lt = bs_less(key, bk);
 #pragma unroll
-                for (int i = 0; i < Cfg::NK; ++i) bk[i] = (key[i] & lt) | (bk[i] & ~lt);
+                for (int i = 0; i < Cfg::NK; ++i) bk[i] = bs_select(key[i], bk[i], lt);
 #pragma unroll
-                for (int k = 0; k < W; ++k) bsl[k] = (sl[k] & lt) | (bsl[k] & ~lt);
+                for (int k = 0; k < W; ++k) bsl[k] = bs_select(sl[k], bsl[k], lt);
             }
         }
         // commit: ones(best) <= popcount(S)  (general form of fsm_step4)
