@@ -363,7 +363,7 @@ def run_ours(args, rank, world, local_rank):
         # free the device-resident copy so the host path owns device memory
         del text, pattern
         torch.cuda.empty_cache()
-        for _ in range(1):
+        for _ in range(max(1, args.warmup)):  # same W untimed steps as the device phase
             pf.shouji_filter_batch(tn, pn, e, ctx=ctx)
         if world > 1:
             dist.barrier()
@@ -383,6 +383,7 @@ def run_ours(args, rank, world, local_rank):
                "d2h_bytes_per_step": (x1[1] - x0[1]) // args.steps,
                "ascii_bytes_per_step": int(2 * n * m),
                "ms_per_step": 1e3 * e2e_s,
+               "step_ms": [round(1e3 * x, 2) for x in tw],
                "path": "pf_shouji_filter_batch(pinned host ASCII records, stride=m): host cores pack "
                        "2-bit dibit records (N planes only for chunks with an N) chunk by chunk into "
                        "pinned buffers, H2D, device pack + search kernels, D2H accept bitmap, sync"
