@@ -173,10 +173,26 @@ def cpu_baseline(text, pattern, e, target_s, threads=None):
             lib.shouji_batch(t, p, e, threads=threads, estimates=False)
             times.append(time.perf_counter() - t0)
     med = float(np.median(times))
-    return {"value": n / med, "unit": UNIT, "cores": int(threads), "kind": kind,
-            "sample": f"first {n} pairs of this run's workload (m={text.shape[1]}, E={e}), "
-                      f"pre-packed, median of 3 passes after 1 warm-up, {threads} threads "
-                      f"(parallel_for_pairs), CPU: {lscpu_model()}"}
+    out = {"value": n / med, "unit": UNIT, "cores": int(threads), "kind": kind,
+           "sample": f"first {n} pairs of this run's workload (m={text.shape[1]}, E={e}), "
+                     f"pre-packed, median of 3 passes after 1 warm-up, {threads} threads "
+                     f"(parallel_for_pairs), CPU: {lscpu_model()}"}
+    if kind == "reference" and threads > 1:
+        # also at T = 1 (bench.hpp:17-19), on a 1/threads-sized sample
+        n1 = max(1, n // int(threads))
+        packed = lib.pack(text[:n1], pattern[:n1])
+        try:
+            packed.shouji(e, threads=1, estimates=False)
+            t1 = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                packed.shouji(e, threads=1, estimates=False)
+                t1.append(time.perf_counter() - t0)
+        finally:
+            packed.free()
+        out["value_1thread"] = n1 / float(np.median(t1))
+        out["sample_1thread"] = f"first {n1} pairs, 1 thread, median of 3 after 1 warm-up"
+    return out
 
 
 def reference_workload(n, m, e, seed):
