@@ -260,7 +260,8 @@ __device__ __forceinline__ void finish_group(const uint32_t (&cnt)[NC], long lon
 }
 
 // The whole Shouji sweep for group g (32 pairs) from its planes.
-template <int E, bool NCLOAD>
+// NC: bit planes of the estimate counter (8: m <= 255, 12: m <= 4095).
+template <int E, bool NCLOAD, int NC = 8>
 __device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes, long long g,
                                              long long n, int m, uint32_t* __restrict__ accept,
                                              uint32_t* __restrict__ estimates,
@@ -268,7 +269,6 @@ __device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes
     using Cfg = SearchCfg<E>;
     constexpr int B = Cfg::B;
     constexpr bool CARRY = Cfg::CARRY;
-    constexpr int NC = 8;  // counter planes: estimates up to 255 (m <= 255 here)
     constexpr int COLW = 3 * kPackGroups;  // words per column of one group's planes
     const long long row0 = g * 32;
     if (row0 >= n) return;
@@ -358,7 +358,7 @@ __device__ __forceinline__ void fetch_col(uint32_t* dst, const uint32_t* __restr
     }
 }
 
-template <int E>
+template <int E, int NC = 8>
 __device__ __forceinline__ void search_group_pf(const uint32_t* __restrict__ planes, long long g,
                                                 long long n, int m, uint32_t* __restrict__ accept,
                                                 uint32_t* __restrict__ estimates,
@@ -367,7 +367,6 @@ __device__ __forceinline__ void search_group_pf(const uint32_t* __restrict__ pla
     using P = PfCfg<E>;
     constexpr int B = 4;
     constexpr int R = P::R;
-    constexpr int NC = 8;
     const long long row0 = g * 32;
     const long long ngroups = (n + 31) / 32;
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
@@ -471,30 +470,30 @@ __device__ __forceinline__ void search_group_pf(const uint32_t* __restrict__ pla
     if (live) finish_group<E>(cnt, row0, n, g, accept, estimates);
 }
 
-template <int E>
+template <int E, int NC>
 __global__ void __launch_bounds__(SearchCfg<E>::NT, SearchCfg<E>::MINB)
 shouji_search_w4_pf(const uint32_t* __restrict__ planes, long long n, int m,
                     uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
                     uint32_t* __restrict__ outplanes) {
     extern __shared__ uint32_t pf_smem[];
     const long long g = static_cast<long long>(blockIdx.x) * SearchCfg<E>::NT + threadIdx.x;
-    search_group_pf<E>(planes, g, n, m, accept, estimates, outplanes,
-                       pf_smem + threadIdx.x * PfCfg<E>::WORDS);
+    search_group_pf<E, NC>(planes, g, n, m, accept, estimates, outplanes,
+                           pf_smem + threadIdx.x * PfCfg<E>::WORDS);
 }
 
 bool search_prefetch_enabled();
 
-template <int E>
+template <int E, int NC>
 __global__ void __launch_bounds__(SearchCfg<E>::NT, SearchCfg<E>::MINB)
 shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
                  uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
                  uint32_t* __restrict__ outplanes) {
     const long long g = static_cast<long long>(blockIdx.x) * SearchCfg<E>::NT + threadIdx.x;
-    search_group<E, true>(planes, g, n, m, accept, estimates, outplanes);
+    search_group<E, true, NC>(planes, g, n, m, accept, estimates, outplanes);
 }
 
-template <int E>
-cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s) {
+template <int E, int NC>
+cudaError_t launch_search_nc(const FilterArgs& a, cudaStream_t s) {
     using Cfg = SearchCfg<E>;
     const long long ngroups = (a.n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + Cfg::NT - 1) / Cfg::NT);
@@ -505,18 +504,25 @@ cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s) {
         if (search_prefetch_enabled()) {
             const size_t smem = static_cast<size_t>(Cfg::NT) * PfCfg<E>::WORDS * 4;
             const cudaError_t st =
-                ensure_smem_attr<shouji_search_w4_pf<E>>(static_cast<int>(smem));
+                ensure_smem_attr<shouji_search_w4_pf<E, NC>>(static_cast<int>(smem));
             if (st != cudaSuccess) return st;
-            shouji_search_w4_pf<E><<<grid, Cfg::NT, smem, s>>>(a.planes, a.n, a.m, a.accept,
-                                                              a.estimates, a.outplanes);
+            shouji_search_w4_pf<E, NC><<<grid, Cfg::NT, smem, s>>>(a.planes, a.n, a.m, a.accept,
+                                                                  a.estimates, a.outplanes);
             count_launch();
             return cudaGetLastError();
         }
     }
-    shouji_search_w4<E><<<grid, Cfg::NT, 0, s>>>(a.planes, a.n, a.m, a.accept, a.estimates,
-                                                  a.outplanes);
+    shouji_search_w4<E, NC><<<grid, Cfg::NT, 0, s>>>(a.planes, a.n, a.m, a.accept, a.estimates,
+                                                      a.outplanes);
     count_launch();
     return cudaGetLastError();
+}
+
+// The counter width follows m: 8 planes up to m = 255 (the common case, fewer
+// live registers), 12 planes up to 4095.
+template <int E>
+cudaError_t launch_search_e(const FilterArgs& a, cudaStream_t s) {
+    return a.m <= 255 ? launch_search_nc<E, 8>(a, s) : launch_search_nc<E, 12>(a, s);
 }
 
 }  // namespace sb

@@ -269,8 +269,9 @@ static cudaError_t launch_generic(const FilterArgs& a, cudaStream_t s) {
 
 size_t planes_scratch_words(long long n, int m) { return plane_words(n, m); }
 
+// The width-4 kernels count estimates in 12 bit planes (m <= 4095).
 bool use_fused(uint32_t width, uint32_t e, int m) {
-    return width == 4 && e <= static_cast<uint32_t>(kFusedMaxE) && m <= 255;
+    return width == 4 && e <= static_cast<uint32_t>(kFusedMaxE) && m <= 4095;
 }
 
 cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {

@@ -445,3 +445,21 @@ def test_profile_stages(gpu):
     ref = torch.zeros_like(acc)
     gpu.shouji_filter_device(tt.data_ptr(), pt.data_ptr(), pitch, n, m, e, ref.data_ptr())
     assert torch.equal(acc, ref)
+
+
+@pytest.mark.parametrize("m", [256, 300, 600, 1000])
+def test_width4_long_records(gpu, oracle, m):
+    """m in (255, 4095]: the width-4 kernels with the 12-plane counter (estimates above
+    255 on random pairs), against the oracle."""
+    rng = np.random.default_rng(m)
+    n = 1500
+    t = np.frombuffer(b"ACGTN", np.uint8)[rng.integers(0, 5, size=(n, m))]
+    p = t.copy()
+    half = n // 2
+    p[half:] = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=(n - half, m))]
+    mask = rng.random((half, m)) < 0.05
+    p[:half][mask] = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=int(mask.sum()))]
+    for e in (3, 12, 25, 31):
+        a, est = check_batch(gpu, oracle, t, p, e)
+        if m >= 1000:
+            assert est.max() > 255  # the counter really goes past 8 planes
