@@ -235,6 +235,16 @@ static constexpr std::array<SearchFn, sizeof...(Es)> make_search_table(std::inte
 static constexpr auto kSearchTable =
     make_search_table(std::make_integer_sequence<int, kFusedMaxE + 1>{});
 
+// Blocked any-width search (wsearch.cuh) instead of the per-column generic
+// kernel: PF_WSEARCH=0 turns it off (A/B runs).
+static bool wsearch_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("PF_WSEARCH");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 // Prefetching search (fused.cuh shouji_search_w4_pf): PF_SEARCH_PF=0 turns it off.
 bool search_prefetch_enabled() {
     static const bool v = [] {
@@ -289,6 +299,7 @@ cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
         if (st != cudaSuccess) return st;
     }
     if (use_fused(a.width, a.e, a.m)) return kSearchTable[a.e](a, s);
+    if (wsearch_enabled() && wsearch_applies(a)) return launch_wsearch(a, s);
     return a.m <= 255 ? launch_generic<8>(a, s) : launch_generic<24>(a, s);
 }
 

@@ -63,6 +63,9 @@ cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitc
 bool nibble_pack_fits(int m);
 cudaError_t launch_pack_nibbles(const uint8_t* text, const uint8_t* pattern, long long n, int m,
                                 uint32_t* planes, cudaStream_t s);
+// Blocked search for any width 3..8 and any E (wsearch.cuh), m <= 4095.
+bool wsearch_applies(const FilterArgs& a);
+cudaError_t launch_wsearch(const FilterArgs& a, cudaStream_t s);
 // Stage 1 from dibit records (+ optional N-plane records; pack.cuh).
 bool dibit_pack_fits(int m);
 cudaError_t launch_pack_dibits(const uint8_t* text, const uint8_t* pattern, const uint8_t* ntext,
