@@ -437,6 +437,12 @@ def run_ours(args, rank, world, local_rank):
                 "kernel_ms_avg": kern_avg_ms}
     if stage_ms is not None:
         pk_ms, se_ms = stage_ms
+        pack_traffic = None
+        try:
+            tj = json.load(open(tpath))
+            pack_traffic = float(tj["per_kernel_bytes"]["pack_tile_kernel<8,4,0>"]) * n / float(tj["pairs"])
+        except Exception:
+            pack_traffic = None
         pack_bytes = n * (2 * m + 2 * 3 * m * 4 / 32)  # ASCII in, 3 planes x 2 sequences out
         # algorithmic LOP3 of the search per 32-pair group and window: map 3 + key 5 per
         # diagonal, compare 4 + mux 7 per diagonal after the first, commit FSM + tally 17
@@ -446,7 +452,8 @@ def run_ours(args, rank, world, local_rank):
             {"kernel": "sb::pack_tile_kernel<8,4,0>", "ms": pk_ms, "share": pk_ms / (pk_ms + se_ms),
              "bound": "hbm", "algorithmic_bytes_per_pair": pack_bytes / n,
              "achieved": pack_bytes / (pk_ms * 1e-3) / 1e9, "unit": "GB/s",
-             "frac": pack_bytes / (pk_ms * 1e-3) / 1e9 / float(peaks["hbm_gbs"])},
+             "frac": pack_bytes / (pk_ms * 1e-3) / 1e9 / float(peaks["hbm_gbs"]),
+             "traffic": pack_traffic},
             {"kernel": f"sb::shouji_search_w4<{e}>", "ms": se_ms, "share": se_ms / (pk_ms + se_ms),
              "bound": "int (ALU pipe, LOP3)", "algorithmic_lop3_per_pair": lop3_pair,
              "achieved": lop3_pair * n / (se_ms * 1e-3), "unit": "lane-ops/s"},
@@ -471,6 +478,21 @@ def run_ours(args, rank, world, local_rank):
                             float(peaks["hbm_gbs"]) * 1e9 / (2 * m + 1 / 8)}
         except Exception as ex:  # diagnostic only
             int_view = {"error": str(ex)}
+
+    # The contract's roofline is the DOMINANT kernel's: when the pack kernel (HBM-bound)
+    # takes the larger share of the step it becomes the top-level object; the whole-step
+    # view is kept under "step".
+    if "per_kernel" in roofline:
+        pk = roofline["per_kernel"][0]
+        if pk["share"] >= 0.5:
+            step_view = {k: v for k, v in roofline.items() if k != "per_kernel"}
+            roofline = {"bound": "hbm", "achieved": pk["achieved"], "peak": float(peaks["hbm_gbs"]),
+                        "unit": "GB/s", "frac": pk["frac"], "traffic": pk["traffic"],
+                        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                        "kernel": pk["kernel"], "share_of_step": pk["share"],
+                        "algorithmic_bytes_per_pair": pk["algorithmic_bytes_per_pair"],
+                        "kernel_ms_avg": pk["ms"], "per_kernel": roofline["per_kernel"],
+                        "step": step_view}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
