@@ -311,7 +311,7 @@ __device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes
     finish_group<E>(cnt, row0, n, g, accept, estimates);
 }
 
-// ---- prefetching form (CARRY, used for 7 <= E <= 12) ---------------------------
+// ---- prefetching form (CARRY, used for 8 <= E <= 12) ---------------------------
 // The same sweep, but the planes a block needs arrive one block ahead with
 // cp.async into a per-thread shared-memory region: a double-buffered text
 // slot (4 columns x 3 planes) and a pattern ring of R = 2E+8 columns (block
@@ -498,9 +498,10 @@ cudaError_t launch_search_nc(const FilterArgs& a, cudaStream_t s) {
     const long long ngroups = (a.n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + Cfg::NT - 1) / Cfg::NT);
     // measured on B200 (tools/exp_e_sweep.py, m=100): the prefetching form wins
-    // from E = 7 (+1%) to E = 12 (+7% at E = 10) and loses below (its per-block
-    // fetch bookkeeping outweighs the hidden latency when there are few diagonals)
-    if constexpr (Cfg::CARRY && E >= 7) {
+    // from E = 8 (+5%) to E = 12 (+7% at E = 10), ties at E = 7 and loses below
+    // (its per-block fetch bookkeeping outweighs the hidden latency when there
+    // are few diagonals)
+    if constexpr (Cfg::CARRY && E >= 8) {
         if (search_prefetch_enabled()) {
             const size_t smem = static_cast<size_t>(Cfg::NT) * PfCfg<E>::WORDS * 4;
             const cudaError_t st =
