@@ -401,12 +401,13 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     }
 
     // ---- host -> device ----------------------------------------------------
-    // Records land in the device layout (pitch = round4(m)). A caller buffer
-    // already in that layout is one DMA per sequence; otherwise rows are
-    // streamed in chunks: contiguous DMA of the caller's rows into a device
-    // staging slot, then a repitch kernel. Pageable input first goes through a
-    // double-buffered pinned staging copy (host memcpy of chunk i+1 overlaps the
-    // DMA of chunk i).
+    // Records land in the device layout (pitch = round4(m), or the caller's
+    // 4-byte-multiple stride for pinned buffers). Pinned records already in that
+    // layout are one DMA per sequence; other pinned strides are DMA'd
+    // contiguously into a device staging slot and re-pitched by a kernel.
+    // Pageable records are copied row by row into double-buffered pinned
+    // staging at the device pitch (the host copy of chunk i+1 overlaps the DMA
+    // of chunk i) and DMA'd straight into place.
     const uint8_t* tsrc = text + p0 * stride;
     const uint8_t* psrc = pattern + p0 * stride;
     if (pinned && stride == pitch) {
@@ -416,60 +417,62 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         if (!cu(xfer(d.d_pattern, psrc, bytes, cudaMemcpyHostToDevice, d.stream),
                 "H2D pattern"))
             return;
+    } else if (pinned) {
+        const size_t rows = std::max<size_t>(1, std::min(n, kStageBytes / stride));
+        if (!cu(grow(d.d_stage, d.d_stage_bytes, 2 * rows * stride), "alloc device stage")) return;
+        for (size_t r0 = 0; r0 < n; r0 += rows) {
+            const size_t nr = std::min(rows, n - r0);
+            const size_t bytes = (nr - 1) * stride + m;
+            uint8_t* dt = d.d_stage;
+            uint8_t* dp = d.d_stage + rows * stride;
+            if (!cu(xfer(dt, tsrc + r0 * stride, bytes, cudaMemcpyHostToDevice, d.stream),
+                    "H2D text"))
+                return;
+            if (!cu(xfer(dp, psrc + r0 * stride, bytes, cudaMemcpyHostToDevice, d.stream),
+                    "H2D pattern"))
+                return;
+            if (!cu(sb::launch_repitch(dt, stride, d.d_text + r0 * pitch, pitch,
+                                       static_cast<long long>(nr), static_cast<int>(m), d.stream),
+                    "repitch text"))
+                return;
+            if (!cu(sb::launch_repitch(dp, stride, d.d_pattern + r0 * pitch, pitch,
+                                       static_cast<long long>(nr), static_cast<int>(m), d.stream),
+                    "repitch pattern"))
+                return;
+        }
     } else {
-        const size_t sstride = pinned ? stride : m;  // row stride of what is DMA'd
-        const size_t rows = std::max<size_t>(1, std::min(n, kStageBytes / sstride));
-        if (!cu(grow(d.d_stage, d.d_stage_bytes, 2 * rows * sstride), "alloc device stage")) return;
-        if (!pinned) {
-            const size_t need = rows * m * 2;
-            if (d.stage_bytes < need) {
-                for (int b = 0; b < 2; ++b) {
-                    if (d.h_stage[b]) cudaFreeHost(d.h_stage[b]);
-                    d.h_stage[b] = nullptr;
-                    if (!cu(cudaHostAlloc(&d.h_stage[b], need, cudaHostAllocPortable), "alloc stage"))
-                        return;
-                    if (!d.stage_ev[b] &&
-                        !cu(cudaEventCreateWithFlags(&d.stage_ev[b], cudaEventDisableTiming), "event"))
-                        return;
-                }
-                d.stage_bytes = need;
+        const size_t rows = std::max<size_t>(1, std::min(n, kStageBytes / pitch));
+        const size_t need = rows * pitch * 2;
+        if (d.stage_bytes < need) {
+            for (int b = 0; b < 2; ++b) {
+                if (d.h_stage[b]) cudaFreeHost(d.h_stage[b]);
+                d.h_stage[b] = nullptr;
+                if (!cu(cudaHostAlloc(&d.h_stage[b], need, cudaHostAllocPortable), "alloc stage"))
+                    return;
+                if (!d.stage_ev[b] &&
+                    !cu(cudaEventCreateWithFlags(&d.stage_ev[b], cudaEventDisableTiming), "event"))
+                    return;
             }
+            d.stage_bytes = need;
         }
         int buf = 0;
         for (size_t r0 = 0; r0 < n; r0 += rows, buf ^= 1) {
             const size_t nr = std::min(rows, n - r0);
-            const uint8_t* st;
-            const uint8_t* sp;
-            if (pinned) {
-                st = tsrc + r0 * stride;
-                sp = psrc + r0 * stride;
-            } else {
-                if (!cu(cudaEventSynchronize(d.stage_ev[buf]), "stage wait")) return;
-                uint8_t* ht = d.h_stage[buf];
-                uint8_t* hp = ht + rows * m;
-                for (size_t r = 0; r < nr; ++r) {
-                    std::memcpy(ht + r * m, tsrc + (r0 + r) * stride, m);
-                    std::memcpy(hp + r * m, psrc + (r0 + r) * stride, m);
-                }
-                st = ht;
-                sp = hp;
+            if (!cu(cudaEventSynchronize(d.stage_ev[buf]), "stage wait")) return;
+            uint8_t* ht = d.h_stage[buf];
+            uint8_t* hp = ht + rows * pitch;
+            for (size_t r = 0; r < nr; ++r) {
+                std::memcpy(ht + r * pitch, tsrc + (r0 + r) * stride, m);
+                std::memcpy(hp + r * pitch, psrc + (r0 + r) * stride, m);
             }
-            const size_t bytes = (nr - 1) * sstride + m;
-            uint8_t* dt = d.d_stage;
-            uint8_t* dp = d.d_stage + rows * sstride;
-            if (!cu(xfer(dt, st, bytes, cudaMemcpyHostToDevice, d.stream), "H2D text"))
+            const size_t bytes = (nr - 1) * pitch + m;
+            if (!cu(xfer(d.d_text + r0 * pitch, ht, bytes, cudaMemcpyHostToDevice, d.stream),
+                    "H2D text"))
                 return;
-            if (!cu(xfer(dp, sp, bytes, cudaMemcpyHostToDevice, d.stream), "H2D pattern"))
+            if (!cu(xfer(d.d_pattern + r0 * pitch, hp, bytes, cudaMemcpyHostToDevice, d.stream),
+                    "H2D pattern"))
                 return;
-            if (!pinned && !cu(cudaEventRecord(d.stage_ev[buf], d.stream), "stage record")) return;
-            if (!cu(sb::launch_repitch(dt, sstride, d.d_text + r0 * pitch, pitch,
-                                       static_cast<long long>(nr), static_cast<int>(m), d.stream),
-                    "repitch text"))
-                return;
-            if (!cu(sb::launch_repitch(dp, sstride, d.d_pattern + r0 * pitch, pitch,
-                                       static_cast<long long>(nr), static_cast<int>(m), d.stream),
-                    "repitch pattern"))
-                return;
+            if (!cu(cudaEventRecord(d.stage_ev[buf], d.stream), "stage record")) return;
         }
     }
 
@@ -491,30 +494,49 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     a.planes_words = d.scratch_words;
     const bool short_circuit = e >= m;
     const bool bad_width = !dist && !magnet && (width < 3 || width > 8);
-    if (short_circuit || bad_width || dist || magnet) {
-        if (!cu(sb::launch_validate(a, d.stream), "validate")) return;
-    } else {
-        if (!cu(launch_any(d, a, d.stream), "filter kernel")) return;
-    }
-    uint32_t flag = 0;
-    if (!cu(xfer(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, d.stream),
-            "D2H flag"))
-        return;
-    if (!cu(cudaStreamSynchronize(d.stream), "sync")) return;
-    if (flag) {
+    auto report_illegal = [&]() {
         const unsigned long long init = ~0ull;
         if (!cu(cudaMemcpy(d.d_key, &init, sizeof(init), cudaMemcpyHostToDevice), "key init")) return;
         if (!cu(sb::launch_locate(d.d_text, d.d_pattern, pitch, a.n, a.m, d.d_key, d.stream),
                 "locate"))
             return;
         unsigned long long key = 0;
-        if (!cu(xfer(&key, d.d_key, sizeof(key), cudaMemcpyDeviceToHost, d.stream),
-                "D2H key"))
+        if (!cu(xfer(&key, d.d_key, sizeof(key), cudaMemcpyDeviceToHost, d.stream), "D2H key"))
             return;
         if (!cu(cudaStreamSynchronize(d.stream), "sync")) return;
         decode_illegal(key, static_cast<long long>(p0), tsrc, psrc, stride, true, err);
-        return fail(PF_ERR_ILLEGAL_CHARACTER);
+        fail(PF_ERR_ILLEGAL_CHARACTER);
+    };
+    if (!(short_circuit || bad_width || dist || magnet)) {
+        // the filter itself: kernels, error flag and results in one round trip;
+        // on an illegal byte the results are discarded and the byte located
+        if (!cu(launch_any(d, a, d.stream), "filter kernel")) return;
+        if (bits &&
+            !cu(sb::launch_bits_transpose(d.d_outplanes, a.n, a.m, d.d_bits, d.stream), "bits"))
+            return;
+        uint32_t flag = 0;
+        if (!cu(xfer(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, d.stream), "D2H flag"))
+            return;
+        if (!cu(xfer(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
+                     cudaMemcpyDeviceToHost, d.stream), "D2H accept"))
+            return;
+        if (estimates && !cu(xfer(estimates + p0, d.d_est, n * sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, d.stream), "D2H estimates"))
+            return;
+        if (bits && !cu(xfer(bits + p0 * wpp, d.d_bits, n * wpp * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, d.stream), "D2H bits"))
+            return;
+        if (!cu(cudaStreamSynchronize(d.stream), "sync")) return;
+        if (flag) report_illegal();
+        return;
     }
+    if (!cu(sb::launch_validate(a, d.stream), "validate")) return;
+    uint32_t flag = 0;
+    if (!cu(xfer(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, d.stream),
+            "D2H flag"))
+        return;
+    if (!cu(cudaStreamSynchronize(d.stream), "sync")) return;
+    if (flag) return report_illegal();
     if (bad_width) return;  // caller reports invalid parameters after all shards validated
     if (dist) {
         int32_t* dd = reinterpret_cast<int32_t*>(d.d_est);
@@ -539,9 +561,6 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
                                   d.d_accept, estimates ? d.d_est : nullptr,
                                   bits ? d.d_bits : nullptr, d.stream),
                 "magnet kernel"))
-            return;
-    } else if (bits) {
-        if (!cu(sb::launch_bits_transpose(d.d_outplanes, a.n, a.m, d.d_bits, d.stream), "bits"))
             return;
     }
 
