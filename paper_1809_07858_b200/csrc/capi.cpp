@@ -261,7 +261,9 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     const bool host_pack = hp_mode != 0 && !dist && !magnet && e < m && width >= 3 && width <= 8 && !bits &&
                            (host_format_dibit() ? sb::dibit_pack_fits(static_cast<int>(m))
                                                 : sb::nibble_pack_fits(static_cast<int>(m))) &&
-                           (hp_mode == 1 || static_cast<long long>(n) >= kHostPackMin);
+                           (hp_mode == 1 || (static_cast<long long>(n) >= kHostPackMin &&
+                                             // the portable packer is slower than PCIe
+                                             sb::host_pack_uses_simd()));
     if (!host_pack) {
         if (!cu(grow(d.d_text, d.in_bytes, n * pitch), "alloc text")) return;
         if (!cu(grow(d.d_pattern, d.in_pattern_bytes, n * pitch), "alloc pattern")) return;
