@@ -258,9 +258,14 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         return false;
     };
     const int hp_mode = host_pack_mode();
-    const bool host_pack = hp_mode != 0 && !dist && !magnet && e < m && width >= 3 && width <= 8 && !bits &&
-                           (host_format_dibit() ? sb::dibit_pack_fits(static_cast<int>(m))
-                                                : sb::nibble_pack_fits(static_cast<int>(m))) &&
+    // MAGNET reads the dibit records directly (no pack kernel), so it only
+    // needs the dibit format and its own length limit.
+    const bool shape_ok =
+        magnet ? host_format_dibit() && sb::magnet_supported(static_cast<int>(m))
+               : width >= 3 && width <= 8 && !bits &&
+                     (host_format_dibit() ? sb::dibit_pack_fits(static_cast<int>(m))
+                                          : sb::nibble_pack_fits(static_cast<int>(m)));
+    const bool host_pack = hp_mode != 0 && !dist && e < m && shape_ok &&
                            (hp_mode == 1 || (static_cast<long long>(n) >= kHostPackMin &&
                                              // the portable packer is slower than PCIe
                                              sb::host_pack_uses_simd()));
@@ -284,9 +289,10 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     }
 
     // ---- host packing upload path ---------------------------------------------
-    // The host's cores pack records into nibble records (host_pack.cpp, half
-    // the bytes) chunk by chunk into pinned buffers; chunk i's DMA, device pack
-    // and search run on the stream while the cores pack chunk i+1.
+    // The host's cores pack records into dibit (or nibble) records
+    // (host_pack.cpp) chunk by chunk into pinned buffers; chunk i's DMA, device
+    // pack and search (or the MAGNET kernel, straight from the dibit records)
+    // run on the stream while the cores pack chunk i+1.
     if (host_pack) {
         const bool dib = host_format_dibit();
         // pairs per chunk; a multiple of 256 so the pattern rows (at chunk * rp)
@@ -326,7 +332,8 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
                 !cu(cudaEventCreateWithFlags(&d.nib_ev[b], cudaEventDisableTiming), "event"))
                 return;
         }
-        if (!cu(grow(d.d_scratch, d.scratch_words, sb::planes_scratch_words(chunk, m)),
+        if (!magnet &&
+            !cu(grow(d.d_scratch, d.scratch_words, sb::planes_scratch_words(chunk, m)),
                 "alloc planes"))
             return;
         const uint8_t* tsrc0 = text + p0 * stride;
@@ -372,6 +379,18 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
                     return;
             }
             if (!cu(cudaEventRecord(d.nib_ev[b], d.stream), "record event")) return;
+            if (magnet) {
+                if (!cu(sb::launch_magnet_dibits(
+                            d.d_nib[b], d.d_nib[b] + static_cast<size_t>(chunk) * rp,
+                            has_n ? d.d_nrow[b] : nullptr,
+                            has_n ? d.d_nrow[b] + static_cast<size_t>(chunk) * npr : nullptr, cn,
+                            static_cast<int>(m), static_cast<int>(e), d.d_accept + lo / 32,
+                            estimates ? d.d_est + lo : nullptr,
+                            bits ? d.d_bits + static_cast<size_t>(lo) * wpp : nullptr, d.stream),
+                        "magnet kernel"))
+                    return;
+                continue;
+            }
             sb::FilterArgs a{};
             a.text = d.d_nib[b];
             a.pattern = d.d_nib[b] + static_cast<size_t>(chunk) * rp;
@@ -397,6 +416,9 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         if (estimates &&
             !cu(xfer(estimates + p0, d.d_est, n * sizeof(uint32_t),
                                 cudaMemcpyDeviceToHost, d.stream), "D2H estimates"))
+            return;
+        if (bits && !cu(xfer(bits + p0 * wpp, d.d_bits, n * wpp * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, d.stream), "D2H bits"))
             return;
         cu(cudaStreamSynchronize(d.stream), "sync");
         return;

@@ -99,6 +99,11 @@ bool magnet_supported(int m);
 cudaError_t launch_magnet(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
                           int m, int e, uint32_t* accept, uint32_t* estimates, uint64_t* bits,
                           cudaStream_t s);
+// MAGNET from dibit records (+ optional N-plane rows), as produced by the host pack.
+cudaError_t launch_magnet_dibits(const uint8_t* text, const uint8_t* pattern, const uint8_t* ntext,
+                                 const uint8_t* npattern, long long n, int m, int e,
+                                 uint32_t* accept, uint32_t* estimates, uint64_t* bits,
+                                 cudaStream_t s);
 // e >= m short-circuit outputs.
 cudaError_t launch_accept_all(long long n, int m, uint32_t* accept, uint32_t* estimates,
                               uint64_t* bits, cudaStream_t s);

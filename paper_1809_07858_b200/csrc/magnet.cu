@@ -36,6 +36,9 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "pack.cuh"
+
+#include <type_traits>
 
 namespace sb {
 
@@ -192,10 +195,60 @@ __device__ __forceinline__ void load_planes(const uint8_t* __restrict__ row, int
     }
 }
 
-template <int W>
+// Record sources: where a pair's planes come from. AsciiSrc reads validated
+// ASCII records (pitch bytes per row); DibitSrc reads host-packed dibit records
+// (pack.cuh, 4*ceil(m/16) bytes per row) plus optional N-plane rows.
+struct AsciiSrc {
+    const uint8_t* text;
+    const uint8_t* pattern;
+    size_t pitch;
+    template <int W>
+    __device__ __forceinline__ void load(long long pair, int seq, int m, uint32_t (&lo)[W],
+                                         uint32_t (&hi)[W], uint32_t (&nn)[W]) const {
+        load_planes<W>((seq ? pattern : text) + pair * pitch, m, lo, hi, nn);
+    }
+};
+
+struct DibitSrc {
+    const uint8_t* text;
+    const uint8_t* pattern;
+    const uint8_t* ntext;  // null: no N in the batch
+    const uint8_t* npattern;
+    template <int W>
+    __device__ __forceinline__ void load(long long pair, int seq, int m, uint32_t (&lo)[W],
+                                         uint32_t (&hi)[W], uint32_t (&nn)[W]) const {
+        constexpr uint32_t K = (1u << 24) | (1u << 17) | (1u << 10) | (1u << 3);
+        const size_t dp = dibit_pitch(m), np = nplane_pitch(m);
+        const uint32_t* row =
+            reinterpret_cast<const uint32_t*>((seq ? pattern : text) + pair * dp);
+        const uint8_t* nb = seq ? npattern : ntext;
+        const uint32_t* nrow = nb ? reinterpret_cast<const uint32_t*>(nb + pair * np) : nullptr;
+        const int nw16 = (m + 15) / 16;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            uint32_t a = 0u, b = 0u;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (2 * i + h < nw16) {
+                    const uint32_t w = row[2 * i + h];
+                    // byte q holds columns q, q+4, q+8, q+12 at bit pairs 2t: column 4t+q
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        a |= (((((w >> (2 * t)) & 0x01010101u) * K) >> 24) & 0xFu) << (16 * h + 4 * t);
+                        b |= (((((w >> (2 * t + 1)) & 0x01010101u) * K) >> 24) & 0xFu) << (16 * h + 4 * t);
+                    }
+                }
+            }
+            lo[i] = a;
+            hi[i] = b;
+            nn[i] = (nrow && i < (m + 31) / 32) ? nrow[i] : 0u;
+        }
+    }
+};
+
+template <int W, class Src>
 __global__ void __launch_bounds__(128)
-magnet_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern, size_t pitch,
-              long long n, int m, int e, uint32_t* __restrict__ accept,
+magnet_kernel(Src src, long long n, int m, int e, uint32_t* __restrict__ accept,
               uint32_t* __restrict__ estimates, uint64_t* __restrict__ bits) {
     const long long pair = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool live = pair < n;
@@ -206,8 +259,8 @@ magnet_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ patt
     int est = 0;
     if (live) {
         uint32_t Tlo[W], Thi[W], TN[W], Plo[W], Phi[W], PN[W];
-        load_planes<W>(text + pair * pitch, m, Tlo, Thi, TN);
-        load_planes<W>(pattern + pair * pitch, m, Plo, Phi, PN);
+        src.template load<W>(pair, 0, m, Tlo, Thi, TN);
+        src.template load<W>(pair, 1, m, Plo, Phi, PN);
 #pragma unroll
         for (int i = 0; i < W; ++i) bv[i] = valid[i];
         // explicit pre-order stack of column ranges [lo, hi] (hi may be < lo)
@@ -379,10 +432,9 @@ __device__ __forceinline__ void diag_vector(int d, const uint32_t (&Plo)[W], con
     }
 }
 
-template <int W>
+template <int W, class Src>
 __global__ void __launch_bounds__(kMagnetWarpNT)
-magnet_warp_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
-                   size_t pitch, long long n, int m, int e, uint32_t* __restrict__ accept,
+magnet_warp_kernel(Src src, long long n, int m, int e, uint32_t* __restrict__ accept,
                    uint32_t* __restrict__ estimates, uint64_t* __restrict__ bits) {
     constexpr int kStack = 16 * W + 4;
     __shared__ int16_t st_lo_all[kMagnetWarpNT / 32][kStack];
@@ -409,8 +461,15 @@ magnet_warp_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__
         uint32_t D0[W], D1[W];
         {
             uint32_t Tlo[W], Thi[W], TN[W], Plo[W], Phi[W], PN[W];
-            warp_load_planes<W>(text + pair * pitch, m, lane, Tlo, Thi, TN);
-            warp_load_planes<W>(pattern + pair * pitch, m, lane, Plo, Phi, PN);
+            if constexpr (std::is_same_v<Src, AsciiSrc>) {
+                // the warp converts the row together (lane l: columns 4l, +128, ...)
+                warp_load_planes<W>(src.text + pair * src.pitch, m, lane, Tlo, Thi, TN);
+                warp_load_planes<W>(src.pattern + pair * src.pitch, m, lane, Plo, Phi, PN);
+            } else {
+                // every lane decodes the record itself (same addresses: broadcast loads)
+                src.template load<W>(pair, 0, m, Tlo, Thi, TN);
+                src.template load<W>(pair, 1, m, Plo, Phi, PN);
+            }
 #pragma unroll
             for (int i = 0; i < W; ++i) PN[i] |= ~valid[i];
             if (has0) {
@@ -499,15 +558,14 @@ magnet_warp_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__
     if (lane == 0) accept[group] = acc_word;
 }
 
-template <int W>
-cudaError_t launch_magnet_warp_w(const uint8_t* text, const uint8_t* pattern, size_t pitch,
-                                 long long n, int m, int e, uint32_t* accept, uint32_t* estimates,
-                                 uint64_t* bits, cudaStream_t s) {
+template <int W, class Src>
+cudaError_t launch_magnet_warp_w(const Src& src, long long n, int m, int e, uint32_t* accept,
+                                 uint32_t* estimates, uint64_t* bits, cudaStream_t s) {
     const long long groups = (n + 31) / 32;
     constexpr int wpb = kMagnetWarpNT / 32;
     const unsigned grid = static_cast<unsigned>((groups + wpb - 1) / wpb);
-    magnet_warp_kernel<W><<<grid, kMagnetWarpNT, 0, s>>>(text, pattern, pitch, n, m, e, accept,
-                                                         estimates, bits);
+    magnet_warp_kernel<W, Src><<<grid, kMagnetWarpNT, 0, s>>>(src, n, m, e, accept, estimates,
+                                                              bits);
     count_launch();
     return cudaGetLastError();
 }
@@ -520,14 +578,34 @@ bool magnet_warp_enabled() {
     return v;
 }
 
-template <int W>
-cudaError_t launch_magnet_w(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
-                            int m, int e, uint32_t* accept, uint32_t* estimates, uint64_t* bits,
-                            cudaStream_t s) {
+template <int W, class Src>
+cudaError_t launch_magnet_w(const Src& src, long long n, int m, int e, uint32_t* accept,
+                            uint32_t* estimates, uint64_t* bits, cudaStream_t s) {
     const unsigned grid = static_cast<unsigned>((n + 127) / 128);
-    magnet_kernel<W><<<grid, 128, 0, s>>>(text, pattern, pitch, n, m, e, accept, estimates, bits);
+    magnet_kernel<W, Src><<<grid, 128, 0, s>>>(src, n, m, e, accept, estimates, bits);
     count_launch();
     return cudaGetLastError();
+}
+
+// Kernel choice by E and the register width W = ceil(m/32) (rounded to 1, 2, 4, 8, 16).
+template <class Src>
+cudaError_t launch_magnet_src(const Src& src, long long n, int m, int e, uint32_t* accept,
+                              uint32_t* estimates, uint64_t* bits, cudaStream_t s) {
+    // the warp form pays per-pair setup and a warp reduction per extraction; it
+    // wins once most lanes own a diagonal (measured: m=250 E=15 68 vs 52 M pairs/s,
+    // E=25 38 vs 23; m=100 E=10 219 vs 242, m=150 E=7 110 vs 194)
+    if (e >= 13 && e <= 31 && magnet_warp_enabled()) {
+        if (m <= 32) return launch_magnet_warp_w<1>(src, n, m, e, accept, estimates, bits, s);
+        if (m <= 64) return launch_magnet_warp_w<2>(src, n, m, e, accept, estimates, bits, s);
+        if (m <= 128) return launch_magnet_warp_w<4>(src, n, m, e, accept, estimates, bits, s);
+        if (m <= 256) return launch_magnet_warp_w<8>(src, n, m, e, accept, estimates, bits, s);
+        return launch_magnet_warp_w<16>(src, n, m, e, accept, estimates, bits, s);
+    }
+    if (m <= 32) return launch_magnet_w<1>(src, n, m, e, accept, estimates, bits, s);
+    if (m <= 64) return launch_magnet_w<2>(src, n, m, e, accept, estimates, bits, s);
+    if (m <= 128) return launch_magnet_w<4>(src, n, m, e, accept, estimates, bits, s);
+    if (m <= 256) return launch_magnet_w<8>(src, n, m, e, accept, estimates, bits, s);
+    return launch_magnet_w<16>(src, n, m, e, accept, estimates, bits, s);
 }
 
 }  // namespace
@@ -539,21 +617,17 @@ cudaError_t launch_magnet(const uint8_t* text, const uint8_t* pattern, size_t pi
                           cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     if (!magnet_supported(m) || pitch % 4 != 0 || e < 0 || e >= m) return cudaErrorInvalidValue;
-    // the warp form pays per-pair setup and a warp reduction per extraction; it
-    // wins once most lanes own a diagonal (measured: m=250 E=15 68 vs 52 M pairs/s,
-    // E=25 38 vs 23; m=100 E=10 219 vs 242, m=150 E=7 110 vs 194)
-    if (e >= 13 && e <= 31 && magnet_warp_enabled()) {
-        if (m <= 32) return launch_magnet_warp_w<1>(text, pattern, pitch, n, m, e, accept, estimates, bits, s);
-        if (m <= 64) return launch_magnet_warp_w<2>(text, pattern, pitch, n, m, e, accept, estimates, bits, s);
-        if (m <= 128) return launch_magnet_warp_w<4>(text, pattern, pitch, n, m, e, accept, estimates, bits, s);
-        if (m <= 256) return launch_magnet_warp_w<8>(text, pattern, pitch, n, m, e, accept, estimates, bits, s);
-        return launch_magnet_warp_w<16>(text, pattern, pitch, n, m, e, accept, estimates, bits, s);
-    }
-    if (m <= 32) return launch_magnet_w<1>(text, pattern, pitch, n, m, e, accept, estimates, bits, s);
-    if (m <= 64) return launch_magnet_w<2>(text, pattern, pitch, n, m, e, accept, estimates, bits, s);
-    if (m <= 128) return launch_magnet_w<4>(text, pattern, pitch, n, m, e, accept, estimates, bits, s);
-    if (m <= 256) return launch_magnet_w<8>(text, pattern, pitch, n, m, e, accept, estimates, bits, s);
-    return launch_magnet_w<16>(text, pattern, pitch, n, m, e, accept, estimates, bits, s);
+    return launch_magnet_src(AsciiSrc{text, pattern, pitch}, n, m, e, accept, estimates, bits, s);
+}
+
+cudaError_t launch_magnet_dibits(const uint8_t* text, const uint8_t* pattern, const uint8_t* ntext,
+                                 const uint8_t* npattern, long long n, int m, int e,
+                                 uint32_t* accept, uint32_t* estimates, uint64_t* bits,
+                                 cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (!magnet_supported(m) || e < 0 || e >= m) return cudaErrorInvalidValue;
+    return launch_magnet_src(DibitSrc{text, pattern, ntext, npattern}, n, m, e, accept, estimates,
+                             bits, s);
 }
 
 }  // namespace sb

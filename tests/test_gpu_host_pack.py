@@ -187,3 +187,35 @@ def test_host_batch_chunks_with_and_without_n(gpu, oracle):
     chunk = 1 << 18
     cn = min(chunk, n - chunk)
     assert h1 - h0 == 2 * n * gpu.dibit_pitch(100) + 2 * cn * gpu.nplane_pitch(100)
+
+
+@pytest.mark.parametrize("m,e", [(100, 5), (100, 20), (17, 3), (250, 25), (512, 9)])
+def test_magnet_host_batch_reads_dibits(gpu, oracle, m, e):
+    """MAGNET host batches of >= 65536 pairs run straight from the dibit records
+    (magnet.cu DibitSrc): two dibit rows per pair cross PCIe, and chunks with and
+    without N (N planes uploaded only where present) match the oracle bit for bit."""
+    rng = np.random.default_rng(m * 31 + e)
+    n = 70_000 if m <= 100 else 66_000
+    t, p = mutated(rng, n, m, alphabet=ACGT)
+    t[n - 3, m // 2] = ord("N")  # one N in the only chunk
+    h0, _ = gpu.transfer_bytes()
+    a1, e1, b1 = gpu.magnet_filter_batch(t, p, e, estimates=True, bits=True)
+    h1, _ = gpu.transfer_bytes()
+    assert h1 - h0 == 2 * n * (gpu.dibit_pitch(m) + gpu.nplane_pitch(m))
+    a2, e2, b2 = oracle.magnet_batch(t, p, e, bits=True)
+    assert (e1 == e2).all() and (a1 == a2).all() and (b1 == b2).all()
+
+
+def test_magnet_host_batch_chunks_and_errors(gpu, oracle):
+    rng = np.random.default_rng(99)
+    n, m = 600_000, 100  # three chunks; N only in the second
+    t, p = mutated(rng, n, m, alphabet=ACGT)
+    p[300_000:300_010, 3] = ord("N")
+    a1, e1, _ = gpu.magnet_filter_batch(t, p, 6, estimates=True)
+    a2, e2, _ = oracle.magnet_batch(t, p, 6)
+    assert (e1 == e2).all() and (a1 == a2).all()
+    p[590_000, 5] = ord("x")   # third chunk
+    t[400_000, 99] = ord("-")  # second chunk: reported first
+    with pytest.raises(gpu.illegal_character_error) as ei:
+        gpu.magnet_filter_batch(t, p, 6)
+    assert (ei.value.pair, ei.value.field, ei.value.position()) == (400_000, 0, 99)
