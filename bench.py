@@ -443,11 +443,16 @@ def run_ours(args, rank, world, local_rank):
             pack_traffic = float(tj["per_kernel_bytes"]["pack_tile_kernel<8,4,0>"]) * n / float(tj["pairs"])
         except Exception:
             pack_traffic = None
-        pack_bytes = n * (2 * m + 2 * 3 * m * 4 / 32)  # ASCII in, 3 planes x 2 sequences out
-        # algorithmic LOP3 of the search per 32-pair group and window: map 3 + key 5 per
-        # diagonal, compare 4 + mux 7 per diagonal after the first, commit FSM + tally 17
+        # ASCII in; lo/hi planes x 2 sequences out, plus the N planes unless the pack
+        # skips them (N-presence flags, pack.cuh: the synthetic config-1 data has no N)
+        nflags = os.environ.get("PF_NFLAGS", "1") != "0"
+        pack_bytes = n * (2 * m + 2 * 2 * m / 8 + (0 if nflags else 2 * m / 8))
+        # algorithmic LOP3 of the search per 32-pair group and window: map 2 (N-free
+        # warps; 3 with N planes) + key 4 per diagonal (two windows share a 3-column
+        # popcount), compare 4 + mux 6 per diagonal after the first, commit FSM (incl.
+        # recovering the unselected slice bit) + tally 19
         windows = ((m + 3 + 3) // 4) * 4
-        lop3_pair = ((2 * e + 1) * 8 + 2 * e * 11 + 17) * windows / 32
+        lop3_pair = ((2 * e + 1) * (6 if nflags else 7) + 2 * e * 10 + 19) * windows / 32
         roofline["per_kernel"] = [
             {"kernel": "sb::pack_tile_kernel<8,4,0>", "ms": pk_ms, "share": pk_ms / (pk_ms + se_ms),
              "bound": "hbm", "algorithmic_bytes_per_pair": pack_bytes / n,

@@ -12,7 +12,8 @@
 //     order; each new pattern column is one load per plane (8 threads share
 //     one fully used 32-byte sector), kept in a sliding register window;
 //   * D_d for the block's columns is (Plo^Tlo)|(Phi^Thi)|PN|TN;
-//   * the window key is 2*ones + bit0 and the winner is the strict first
+//   * the window key is 2*ones + bit0 (windows 0,1 and 2,3 of a block share
+//     the popcount of their three common columns) and the winner is the strict first
 //     minimum — exactly select_window's "more zeros, or equal zeros and a
 //     leading zero replacing a leading one" rule;
 //   * commit_window becomes a 3-bit state machine (fsm_step4): bit j+3 is
@@ -36,27 +37,40 @@
 
 namespace sb {
 
+// A window's candidate: the key planes and slice bits 1, 2. The slice's last
+// bit is implied — the low bit of ones is the parity of the four slice bits,
+// so s3 = k1 ^ k0 ^ s1 ^ s2 — and is recovered once per window at commit.
 struct Cand4 {
     uint32_t k[4];  // key planes: k0 = slice bit 0, k1..k3 = ones count
-    uint32_t s[3];  // slice bits 1..3
+    uint32_t s[2];  // slice bits 1..2
 };
 
-__device__ __forceinline__ void make_cand4(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
-                                           Cand4& out) {
-    const uint32_t s1 = a ^ b ^ c;
-    const uint32_t c1 = (a & b) | (a & c) | (b & c);
-    out.k[0] = a;
-    out.k[1] = s1 ^ d;
-    out.k[2] = c1 ^ (s1 & d);
-    out.k[3] = c1 & s1 & d;
-    out.s[0] = b;
-    out.s[1] = c;
-    out.s[2] = d;
+// The four windows of a block over D columns sv[0..6] (window b = sv[b..b+3]).
+// Windows 0,1 share the triple sv[1..3] and windows 2,3 the triple sv[3..5]:
+// ones = triple + the window's outer bit, 4 LOP3 per window instead of 5.
+__device__ __forceinline__ void make_block_cands(const uint32_t (&sv)[7], Cand4 (&cd)[4]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t a = sv[2 * h + 1], b = sv[2 * h + 2], c = sv[2 * h + 3];
+        const uint32_t t0 = lop3<0x96>(a, b, c);  // a ^ b ^ c
+        const uint32_t t1 = lop3<0xE8>(a, b, c);  // majority
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            const int bw = 2 * h + w;
+            const uint32_t x = w == 0 ? sv[2 * h] : sv[2 * h + 4];
+            cd[bw].k[0] = sv[bw];
+            cd[bw].k[1] = t0 ^ x;
+            cd[bw].k[2] = lop3<0x78>(t1, t0, x);  // t1 ^ (t0 & x)
+            cd[bw].k[3] = lop3<0x80>(t1, t0, x);  // t1 & t0 & x
+            cd[bw].s[0] = sv[bw + 1];
+            cd[bw].s[1] = sv[bw + 2];
+        }
+    }
 }
 
 // best = c if key(c) < key(best): 4 LOP3 for the strict compare (LSB first:
-// lt = ~c&b | ~(c^b)&lt, table 0x8E) and 7 for the select (lt ? c : best,
-// table 0xE4) — 11 per candidate, pinned with explicit lop3.
+// lt = ~c&b | ~(c^b)&lt, table 0x8E) and 6 for the select (lt ? c : best,
+// table 0xE4) — 10 per candidate, pinned with explicit lop3.
 __device__ __forceinline__ void update_best4(const Cand4& c, Cand4& best) {
     uint32_t lt = lop3<0x8E>(c.k[0], best.k[0], 0u);
     lt = lop3<0x8E>(c.k[1], best.k[1], lt);
@@ -65,11 +79,12 @@ __device__ __forceinline__ void update_best4(const Cand4& c, Cand4& best) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) best.k[i] = lop3<0xE4>(c.k[i], best.k[i], lt);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) best.s[i] = lop3<0xE4>(c.s[i], best.s[i], lt);
+    for (int i = 0; i < 2; ++i) best.s[i] = lop3<0xE4>(c.s[i], best.s[i], lt);
 }
 
 // commit_window as a state machine over S = tally bits (j, j+1, j+2).
 __device__ __forceinline__ uint32_t fsm_step4(const Cand4& best, uint32_t (&S)[3]) {
+    const uint32_t s3 = lop3<0x96>(best.k[1], best.k[0], best.s[0]) ^ best.s[1];  // ones parity
     const uint32_t p0 = S[0] ^ S[1] ^ S[2];
     const uint32_t p1 = (S[0] & S[1]) | (S[0] & S[2]) | (S[1] & S[2]);
     const uint32_t x0 = ~best.k[1] | p0;
@@ -78,7 +93,7 @@ __device__ __forceinline__ uint32_t fsm_step4(const Cand4& best, uint32_t (&S)[3
     const uint32_t out = (commit & best.k[0]) | (~commit & S[0]);
     S[0] = (commit & best.s[0]) | (~commit & S[1]);
     S[1] = (commit & best.s[1]) | (~commit & S[2]);
-    S[2] = best.s[2] | ~commit;
+    S[2] = s3 | ~commit;
     return out;
 }
 
@@ -92,23 +107,28 @@ struct SearchCfg {
     static constexpr int MINB = E <= 7 ? 4 : 1;
 };
 
-// Column loads relative to a per-block base pointer: word (x*3 + k) * 8 of the
-// group's planes, x counted from the block's first column `col0`. CHECK: the
-// block touches columns outside [0, m), which read as N.
+// Column loads relative to per-block base pointers: lo/hi word (x*2 + k) * 8
+// of base and N word x * 8 of nbase (pack.cuh layout), x counted from the
+// block's first column `col0`. CHECK: the block touches columns outside
+// [0, m), which read as N.
 // NC: the planes are read-only while the search kernel runs (the pack kernel
 // wrote them in an earlier launch), so the non-coherent path may serve them.
-template <bool CHECK, bool NC = true>
-__device__ __forceinline__ void load_rel(const uint32_t* __restrict__ base, int x, int col0, int m,
+// NOPN: the warp's groups are all N-free (N-presence flags, pack.cuh): the N
+// word is 0 and never loaded. (An N-free group in a mixed warp reads an
+// all-zero column image through nbase instead.)
+template <bool CHECK, bool NC = true, bool NOPN = false>
+__device__ __forceinline__ void load_rel(const uint32_t* __restrict__ base,
+                                         const uint32_t* __restrict__ nbase, int x, int col0, int m,
                                          uint32_t (&v)[3]) {
     if (!CHECK || static_cast<unsigned>(col0 + x) < static_cast<unsigned>(m)) {
         if constexpr (NC) {
-            v[0] = __ldg(base + (x * 3 + 0) * kPackGroups);
-            v[1] = __ldg(base + (x * 3 + 1) * kPackGroups);
-            v[2] = __ldg(base + (x * 3 + 2) * kPackGroups);
+            v[0] = __ldg(base + (x * 2 + 0) * kPackGroups);
+            v[1] = __ldg(base + (x * 2 + 1) * kPackGroups);
+            v[2] = NOPN ? 0u : __ldg(nbase + x * kNColWords);
         } else {
-            v[0] = base[(x * 3 + 0) * kPackGroups];
-            v[1] = base[(x * 3 + 1) * kPackGroups];
-            v[2] = base[(x * 3 + 2) * kPackGroups];
+            v[0] = base[(x * 2 + 0) * kPackGroups];
+            v[1] = base[(x * 2 + 1) * kPackGroups];
+            v[2] = NOPN ? 0u : nbase[x * kNColWords];
         }
     } else {
         v[0] = 0u;
@@ -117,25 +137,38 @@ __device__ __forceinline__ void load_rel(const uint32_t* __restrict__ base, int 
     }
 }
 
+// One mismatch-map word D = !bases_match for a (pattern, text) column pair.
+// FAST: both N words are known zero (N-free warp, interior block): 2 LOP3.
+template <bool FAST>
+__device__ __forceinline__ uint32_t map_word(const uint32_t (&p)[3], const uint32_t (&t)[3]) {
+    if constexpr (FAST)
+        return (p[0] ^ t[0]) | (p[1] ^ t[1]);
+    else
+        return (p[0] ^ t[0]) | (p[1] ^ t[1]) | p[2] | t[2];
+}
+
 // Best candidate of each window of one block (windows j0 .. j0+B-1).
 // tcol0/pcol0: first text / pattern column the block reads; tbase/pbase point
 // at those columns (pointers may be out of range when CHECK masks the load).
-template <int E, bool CHECK, bool NC>
-__device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase, int tcol0,
-                                             const uint32_t* __restrict__ pbase, int pcol0, int m,
+template <int E, bool CHECK, bool NC, bool NOPN = false>
+__device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
+                                             const uint32_t* __restrict__ tnbase, int tcol0,
+                                             const uint32_t* __restrict__ pbase,
+                                             const uint32_t* __restrict__ pnbase, int pcol0, int m,
                                              uint32_t (*Dc)[3], Cand4 (&best)[SearchCfg<E>::B]) {
     constexpr int B = SearchCfg<E>::B;
+    constexpr bool FAST = NOPN && !CHECK;
     if constexpr (SearchCfg<E>::CARRY) {
         // new D columns tcol0 .. tcol0+B-1; pattern column = that + d, pcol0 = tcol0 - E
         uint32_t T[B][3];
 #pragma unroll
-        for (int b = 0; b < B; ++b) load_rel<CHECK, NC>(tbase, b, tcol0, m, T[b]);
+        for (int b = 0; b < B; ++b) load_rel<CHECK, NC, NOPN>(tbase, tnbase, b, tcol0, m, T[b]);
         uint32_t P[B][3];
 #pragma unroll
         for (int di = 0; di <= 2 * E; ++di) {
             if (di == 0) {
 #pragma unroll
-                for (int b = 0; b < B; ++b) load_rel<CHECK, NC>(pbase, b, pcol0, m, P[b]);
+                for (int b = 0; b < B; ++b) load_rel<CHECK, NC, NOPN>(pbase, pnbase, b, pcol0, m, P[b]);
             } else {
 #pragma unroll
                 for (int b = 0; b < B - 1; ++b) {
@@ -143,7 +176,7 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
                     P[b][1] = P[b + 1][1];
                     P[b][2] = P[b + 1][2];
                 }
-                load_rel<CHECK, NC>(pbase, B - 1 + di, pcol0, m, P[B - 1]);
+                load_rel<CHECK, NC, NOPN>(pbase, pnbase, B - 1 + di, pcol0, m, P[B - 1]);
             }
             uint32_t s[B + 3];
             s[0] = Dc[di][0];
@@ -151,15 +184,15 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
             s[2] = Dc[di][2];
 #pragma unroll
             for (int b = 0; b < B; ++b)
-                s[3 + b] = (P[b][0] ^ T[b][0]) | (P[b][1] ^ T[b][1]) | P[b][2] | T[b][2];
+                s[3 + b] = map_word<FAST>(P[b], T[b]);
+            Cand4 cd[B];
+            make_block_cands(s, cd);
 #pragma unroll
             for (int b = 0; b < B; ++b) {
-                Cand4 cd;
-                make_cand4(s[b], s[b + 1], s[b + 2], s[b + 3], cd);
                 if (di == 0)
-                    best[b] = cd;
+                    best[b] = cd[b];
                 else
-                    update_best4(cd, best[b]);
+                    update_best4(cd[b], best[b]);
             }
             Dc[di][0] = s[B];
             Dc[di][1] = s[B + 1];
@@ -175,26 +208,25 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
         constexpr int X = B + 3;
         uint32_t T[X][3];
 #pragma unroll
-        for (int x = 0; x < X; ++x) load_rel<CHECK, NC>(tbase, x, tcol0, m, T[x]);
+        for (int x = 0; x < X; ++x) load_rel<CHECK, NC, NOPN>(tbase, tnbase, x, tcol0, m, T[x]);
         uint32_t P[X][3];
 #pragma unroll
-        for (int x = 0; x < X; ++x) load_rel<CHECK, NC>(pbase, x, pcol0, m, P[x]);
+        for (int x = 0; x < X; ++x) load_rel<CHECK, NC, NOPN>(pbase, pnbase, x, pcol0, m, P[x]);
         auto step = [&](const int rot, bool first) {
             // rot = di % X: slot of pattern column pcol0 + di + x is (rot + x) % X
             uint32_t sv[X];
 #pragma unroll
             for (int x = 0; x < X; ++x) {
-                const uint32_t* pp = P[(rot + x) % X];
-                sv[x] = (pp[0] ^ T[x][0]) | (pp[1] ^ T[x][1]) | pp[2] | T[x][2];
+                sv[x] = map_word<FAST>(P[(rot + x) % X], T[x]);
             }
+            Cand4 cd[B];
+            make_block_cands(sv, cd);
 #pragma unroll
             for (int b = 0; b < B; ++b) {
-                Cand4 cd;
-                make_cand4(sv[b], sv[b + 1], sv[b + 2], sv[b + 3], cd);
                 if (first)
-                    best[b] = cd;
+                    best[b] = cd[b];
                 else
-                    update_best4(cd, best[b]);
+                    update_best4(cd[b], best[b]);
             }
         };
         step(0, true);  // di = 0
@@ -205,7 +237,7 @@ __device__ __forceinline__ void search_block(const uint32_t* __restrict__ tbase,
                 const int di = d0 + u;
                 if (di > 2 * E) break;
                 // new column pcol0 + di + X - 1 replaces pcol0 + di - 1 in slot (di - 1) % X = u
-                load_rel<CHECK, NC>(pbase, di + X - 1, pcol0, m, P[u]);
+                load_rel<CHECK, NC, NOPN>(pbase, pnbase, di + X - 1, pcol0, m, P[u]);
                 step((1 + u) % X, false);
             }
         }
@@ -261,22 +293,27 @@ __device__ __forceinline__ void finish_group(const uint32_t (&cnt)[NC], long lon
 
 // The whole Shouji sweep for group g (32 pairs) from its planes.
 // NC: bit planes of the estimate counter (8: m <= 255, 12: m <= 4095).
-template <int E, bool NCLOAD, int NC = 8>
+// NOPN: see load_rel. tzero / pzero: the group's text / pattern N planes are
+// not stored (N-presence flags): read the all-zero column image `zero` instead.
+template <int E, bool NCLOAD, int NC = 8, bool NOPN = false>
 __device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes, long long g,
                                              long long n, int m, uint32_t* __restrict__ accept,
                                              uint32_t* __restrict__ estimates,
-                                             uint32_t* __restrict__ outplanes) {
+                                             uint32_t* __restrict__ outplanes,
+                                             const uint32_t* __restrict__ zero = nullptr,
+                                             bool tzero = false, bool pzero = false) {
     using Cfg = SearchCfg<E>;
     constexpr int B = Cfg::B;
     constexpr bool CARRY = Cfg::CARRY;
-    constexpr int COLW = 3 * kPackGroups;  // words per column of one group's planes
     const long long row0 = g * 32;
     if (row0 >= n) return;
     const long long ngroups = (n + 31) / 32;
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
     const int mc = plane_cols(m);
-    const uint32_t* const tb = planes + plane_index(0, g, 0, 0, nblocks, mc);
-    const uint32_t* const pb = planes + plane_index(1, g, 0, 0, nblocks, mc);
+    const uint32_t* const tb = planes + lohi_index(0, g, 0, 0, nblocks, mc);
+    const uint32_t* const pb = planes + lohi_index(1, g, 0, 0, nblocks, mc);
+    const uint32_t* const tnb = tzero ? zero + g % kPackGroups : planes + nplane_index(0, g, 0, nblocks, mc);
+    const uint32_t* const pnb = pzero ? zero + g % kPackGroups : planes + nplane_index(1, g, 0, nblocks, mc);
 
     constexpr int DCN = CARRY ? 2 * E + 1 : 1;
     uint32_t Dc[DCN][3];
@@ -300,12 +337,16 @@ __device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes
         const bool interior = tcol0 >= 0 && pcol0 >= 0 && tcol0 + TW + E <= m;
         Cand4 best[B];
         // pointers may point outside the group's planes; CHECK masks those loads
-        const uint32_t* tbase = tb + static_cast<long long>(tcol0) * COLW;
-        const uint32_t* pbase = pb + static_cast<long long>(pcol0) * COLW;
+        const uint32_t* tbase = tb + static_cast<long long>(tcol0) * kLhColWords;
+        const uint32_t* pbase = pb + static_cast<long long>(pcol0) * kLhColWords;
+        const uint32_t* tnbase = tnb + static_cast<long long>(tcol0) * kNColWords;
+        const uint32_t* pnbase = pnb + static_cast<long long>(pcol0) * kNColWords;
         if (interior)
-            search_block<E, false, NCLOAD>(tbase, tcol0, pbase, pcol0, m, Dc, best);
+            search_block<E, false, NCLOAD, NOPN>(tbase, tnbase, tcol0, pbase, pnbase, pcol0, m, Dc,
+                                                 best);
         else
-            search_block<E, true, NCLOAD>(tbase, tcol0, pbase, pcol0, m, Dc, best);
+            search_block<E, true, NCLOAD, NOPN>(tbase, tnbase, tcol0, pbase, pnbase, pcol0, m, Dc,
+                                                best);
         commit_block(best, S, j0, m, g, ngroups, outplanes, cnt);
     }
     finish_group<E>(cnt, row0, n, g, accept, estimates);
@@ -343,14 +384,13 @@ struct PfCfg {
 
 // Column `col` of sequence planes `base` (the group's plane words, pack.cuh
 // layout) into dst[0..2]: cp.async in range, N planes outside.
-__device__ __forceinline__ void fetch_col(uint32_t* dst, const uint32_t* __restrict__ base, int col,
-                                          int m) {
-    constexpr int COLW = 3 * kPackGroups;
+__device__ __forceinline__ void fetch_col(uint32_t* dst, const uint32_t* __restrict__ base,
+                                          const uint32_t* __restrict__ nbase, int col, int m) {
     if (static_cast<unsigned>(col) < static_cast<unsigned>(m)) {
-        const uint32_t* src = base + static_cast<long long>(col) * COLW;
+        const uint32_t* src = base + static_cast<long long>(col) * kLhColWords;
         cp_async4(dst + 0, src);
         cp_async4(dst + 1, src + kPackGroups);
-        cp_async4(dst + 2, src + 2 * kPackGroups);
+        cp_async4(dst + 2, nbase + static_cast<long long>(col) * kNColWords);
     } else {
         dst[0] = 0u;
         dst[1] = 0u;
@@ -374,8 +414,10 @@ __device__ __forceinline__ void search_group_pf(const uint32_t* __restrict__ pla
     const bool live = row0 < n;
     // dead threads still walk the blocks (uniform cp.async groups), on group 0's planes
     const long long gg = live ? g : 0;
-    const uint32_t* const tb = planes + plane_index(0, gg, 0, 0, nblocks, mc);
-    const uint32_t* const pb = planes + plane_index(1, gg, 0, 0, nblocks, mc);
+    const uint32_t* const tb = planes + lohi_index(0, gg, 0, 0, nblocks, mc);
+    const uint32_t* const pb = planes + lohi_index(1, gg, 0, 0, nblocks, mc);
+    const uint32_t* const tnb = planes + nplane_index(0, gg, 0, nblocks, mc);
+    const uint32_t* const pnb = planes + nplane_index(1, gg, 0, nblocks, mc);
     uint32_t* const text = region + P::TEXT;
     uint32_t* const ring = region + P::RING;
     auto ring_slot = [&](int col) { return ring + ((col + E) % R) * 3; };
@@ -391,9 +433,9 @@ __device__ __forceinline__ void search_group_pf(const uint32_t* __restrict__ pla
     const int NB = (m + 3 + B - 1) / B;
     // prologue: block 0 (text columns 0..3, pattern columns [-E, 4+E))
 #pragma unroll
-    for (int b = 0; b < B; ++b) fetch_col(text + b * 3, tb, b, m);
+    for (int b = 0; b < B; ++b) fetch_col(text + b * 3, tb, tnb, b, m);
 #pragma unroll 1
-    for (int c = -E; c < B + E; ++c) fetch_col(ring_slot(c), pb, c, m);
+    for (int c = -E; c < B + E; ++c) fetch_col(ring_slot(c), pb, pnb, c, m);
     cp_async_commit();
 #pragma unroll 1
     for (int blk = 0; blk < NB; ++blk) {
@@ -401,11 +443,11 @@ __device__ __forceinline__ void search_group_pf(const uint32_t* __restrict__ pla
         if (blk + 1 < NB) {
             uint32_t* tn = text + ((blk + 1) & 1) * 12;
 #pragma unroll
-            for (int b = 0; b < B; ++b) fetch_col(tn + b * 3, tb, tcol0 + B + b, m);
+            for (int b = 0; b < B; ++b) fetch_col(tn + b * 3, tb, tnb, tcol0 + B + b, m);
 #pragma unroll
             for (int b = 0; b < B; ++b) {
                 const int c = tcol0 + B + E + b;
-                fetch_col(ring_slot(c), pb, c, m);
+                fetch_col(ring_slot(c), pb, pnb, c, m);
             }
         }
         cp_async_commit();
@@ -452,14 +494,14 @@ __device__ __forceinline__ void search_group_pf(const uint32_t* __restrict__ pla
 #pragma unroll
             for (int b = 0; b < B; ++b)
                 sv[3 + b] = (P4[b][0] ^ T[b][0]) | (P4[b][1] ^ T[b][1]) | P4[b][2] | T[b][2];
+            Cand4 cd[B];
+            make_block_cands(sv, cd);
 #pragma unroll
             for (int b = 0; b < B; ++b) {
-                Cand4 cd;
-                make_cand4(sv[b], sv[b + 1], sv[b + 2], sv[b + 3], cd);
                 if (di == 0)
-                    best[b] = cd;
+                    best[b] = cd[b];
                 else
-                    update_best4(cd, best[b]);
+                    update_best4(cd[b], best[b]);
             }
             Dc[di][0] = sv[B];
             Dc[di][1] = sv[B + 1];
@@ -483,13 +525,30 @@ shouji_search_w4_pf(const uint32_t* __restrict__ planes, long long n, int m,
 
 bool search_prefetch_enabled();
 
+// nflags: N-presence flags (pack.cuh) or null. A warp whose 32 groups are all
+// N-free (the usual case) runs the N-free instantiation: no N-plane loads and
+// a 2-LOP3 mismatch map in interior blocks; in a mixed warp the N-free groups
+// read the all-zero column image after the flags.
 template <int E, int NC>
 __global__ void __launch_bounds__(SearchCfg<E>::NT, SearchCfg<E>::MINB)
 shouji_search_w4(const uint32_t* __restrict__ planes, long long n, int m,
                  uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
-                 uint32_t* __restrict__ outplanes) {
+                 uint32_t* __restrict__ outplanes, const uint32_t* __restrict__ nflags) {
     const long long g = static_cast<long long>(blockIdx.x) * SearchCfg<E>::NT + threadIdx.x;
-    search_group<E, true, NC>(planes, g, n, m, accept, estimates, outplanes);
+    if (nflags != nullptr) {
+        const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
+        const bool live = g * 32 < n;
+        const bool tz = !live || nflags[nflag_index(0, g, nblocks)] == 0u;
+        const bool pz = !live || nflags[nflag_index(1, g, nblocks)] == 0u;
+        if (__all_sync(~0u, tz && pz)) {
+            search_group<E, true, NC, true>(planes, g, n, m, accept, estimates, outplanes);
+            return;
+        }
+        search_group<E, true, NC, false>(planes, g, n, m, accept, estimates, outplanes,
+                                         nflags + nflag_words(n), tz, pz);
+        return;
+    }
+    search_group<E, true, NC, false>(planes, g, n, m, accept, estimates, outplanes);
 }
 
 template <int E, int NC>
@@ -502,7 +561,7 @@ cudaError_t launch_search_nc(const FilterArgs& a, cudaStream_t s) {
     // (its per-block fetch bookkeeping outweighs the hidden latency when there
     // are few diagonals)
     if constexpr (Cfg::CARRY && E >= 8) {
-        if (search_prefetch_enabled()) {
+        if (search_prefetch_enabled() && a.nflags == nullptr) {
             const size_t smem = static_cast<size_t>(Cfg::NT) * PfCfg<E>::WORDS * 4;
             const cudaError_t st =
                 ensure_smem_attr<shouji_search_w4_pf<E, NC>>(static_cast<int>(smem));
@@ -514,7 +573,7 @@ cudaError_t launch_search_nc(const FilterArgs& a, cudaStream_t s) {
         }
     }
     shouji_search_w4<E, NC><<<grid, Cfg::NT, 0, s>>>(a.planes, a.n, a.m, a.accept, a.estimates,
-                                                      a.outplanes);
+                                                      a.outplanes, a.nflags);
     count_launch();
     return cudaGetLastError();
 }

@@ -73,10 +73,18 @@ shouji_generic(const uint32_t* __restrict__ planes, long long n, int m, int e,
     const long long row0 = g * 32;
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
     const int mc = plane_cols(m);
-    const uint32_t* tb = planes + plane_index(0, g, 0, 0, nblocks, mc);
-    const uint32_t* pb = planes + plane_index(1, g, 0, 0, nblocks, mc);
-    auto tp = [&](int col, int k) { return __ldg(tb + (size_t(col) * 3 + k) * kPackGroups); };
-    auto pp = [&](int col, int k) { return __ldg(pb + (size_t(col) * 3 + k) * kPackGroups); };
+    const uint32_t* tb = planes + lohi_index(0, g, 0, 0, nblocks, mc);
+    const uint32_t* pb = planes + lohi_index(1, g, 0, 0, nblocks, mc);
+    const uint32_t* tnb = planes + nplane_index(0, g, 0, nblocks, mc);
+    const uint32_t* pnb = planes + nplane_index(1, g, 0, nblocks, mc);
+    auto tp = [&](int col, int k) {
+        return k < 2 ? __ldg(tb + size_t(col) * kLhColWords + k * kPackGroups)
+                     : __ldg(tnb + size_t(col) * kNColWords);
+    };
+    auto pp = [&](int col, int k) {
+        return k < 2 ? __ldg(pb + size_t(col) * kLhColWords + k * kPackGroups)
+                     : __ldg(pnb + size_t(col) * kNColWords);
+    };
 
     uint32_t S[W - 1];
 #pragma unroll
@@ -277,22 +285,47 @@ static cudaError_t launch_generic(const FilterArgs& a, cudaStream_t s) {
     }
 }
 
-size_t planes_scratch_words(long long n, int m) { return plane_words(n, m); }
+size_t planes_scratch_words(long long n, int m) {
+    return plane_words(n, m) + nflag_words(n) + nzero_words(m);
+}
 
 // The width-4 kernels count estimates in 12 bit planes (m <= 4095).
 bool use_fused(uint32_t width, uint32_t e, int m) {
     return width == 4 && e <= static_cast<uint32_t>(kFusedMaxE) && m <= 4095;
 }
 
-cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s) {
-    if (a.n <= 0) return cudaSuccess;
-    if (a.planes == nullptr || a.planes_words < plane_words(a.n, a.m)) return cudaErrorInvalidValue;
+// N-presence flags (pack.cuh): used when the pack kernel can write them and the
+// search is the width-4 kernel (the other searches read every N plane; with
+// flags the direct width-4 form replaces the prefetching one, which it matches
+// or beats at 8 <= E <= 12 once N-free warps drop the N planes: m=100 E8 9.41
+// vs 9.34, E10 8.37 vs 8.30, E12 7.37 vs 7.45 G pairs/s; m=150 E8 5.22 vs
+// 5.09). PF_NFLAGS=0 turns them off (A/B runs).
+static bool nflags_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("PF_NFLAGS");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
+static bool search_reads_nflags(const FilterArgs& a) { return use_fused(a.width, a.e, a.m); }
+
+cudaError_t launch_filter(const FilterArgs& args, cudaStream_t s) {
+    if (args.n <= 0) return cudaSuccess;
+    if (args.planes == nullptr || args.planes_words < plane_words(args.n, args.m))
+        return cudaErrorInvalidValue;
+    FilterArgs a = args;
+    a.nflags = nullptr;
+    if (nflags_enabled() && args.planes_words >= planes_scratch_words(a.n, a.m) &&
+        search_reads_nflags(a) && pack_writes_nflags(a))
+        a.nflags = a.planes + plane_words(a.n, a.m);
     cudaError_t st =
         a.packed_text ? launch_pack_planes(a.packed_text, a.packed_pattern, a.n, a.m, a.planes, s)
         : a.dibits    ? launch_pack_dibits(a.text, a.pattern, a.ntext, a.npattern, a.n, a.m,
-                                           a.planes, s)
-        : a.nibbles   ? launch_pack_nibbles(a.text, a.pattern, a.n, a.m, a.planes, s)
-                      : launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, a.planes, a.err_flag, s);
+                                           a.planes, s, a.nflags)
+        : a.nibbles   ? launch_pack_nibbles(a.text, a.pattern, a.n, a.m, a.planes, s, a.nflags)
+                      : launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, a.planes, a.err_flag, s,
+                                    a.nflags);
     if (st != cudaSuccess) return st;
     if (a.stage_event != nullptr) {
         st = cudaEventRecord(a.stage_event, s);

@@ -50,6 +50,8 @@ struct FilterArgs {
     cudaEvent_t stage_event;   // non-null: recorded between the pack and the search kernel
     const uint64_t* packed_text;     // non-null: pre-packed planes input (pack_planes.cu);
     const uint64_t* packed_pattern;  //   text/pattern/pitch unused
+    uint32_t* nflags;  // set by launch_filter: N-presence flags (pack.cuh) shared by the
+                       // pack and search kernels, or null (N planes always stored and read)
 };
 
 // Scratch words the filter needs for n pairs of length m.
@@ -57,12 +59,16 @@ size_t planes_scratch_words(long long n, int m);
 bool use_fused(uint32_t width, uint32_t e, int m);
 
 // Stage 1: records -> planes (planes may be null: validation only).
+// nflags (optional): write N-presence flags and skip N-free groups' N planes
+// (requires pack_writes_nflags).
 cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
-                        int m, uint32_t* planes, uint32_t* err_flag, cudaStream_t s);
+                        int m, uint32_t* planes, uint32_t* err_flag, cudaStream_t s,
+                        uint32_t* nflags = nullptr);
+bool pack_writes_nflags(const FilterArgs& a);
 // Stage 1 from nibble records (pack.cuh nibble format; no validation).
 bool nibble_pack_fits(int m);
 cudaError_t launch_pack_nibbles(const uint8_t* text, const uint8_t* pattern, long long n, int m,
-                                uint32_t* planes, cudaStream_t s);
+                                uint32_t* planes, cudaStream_t s, uint32_t* nflags = nullptr);
 // Blocked search for any width 3..8 and any E (wsearch.cuh), m <= 4095.
 bool wsearch_applies(const FilterArgs& a);
 cudaError_t launch_wsearch(const FilterArgs& a, cudaStream_t s);
@@ -70,7 +76,8 @@ cudaError_t launch_wsearch(const FilterArgs& a, cudaStream_t s);
 bool dibit_pack_fits(int m);
 cudaError_t launch_pack_dibits(const uint8_t* text, const uint8_t* pattern, const uint8_t* ntext,
                                const uint8_t* npattern, long long n, int m, uint32_t* planes,
-                               cudaStream_t s);
+                               cudaStream_t s,
+                               uint32_t* nflags = nullptr);
 // Stage 1 from packed_sequence planes ([n][3][ceil(m/64)] u64 per sequence).
 cudaError_t launch_pack_planes(const uint64_t* text, const uint64_t* pattern, long long n, int m,
                                uint32_t* planes, cudaStream_t s);

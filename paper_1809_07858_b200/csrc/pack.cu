@@ -12,18 +12,25 @@ namespace sb {
 namespace {
 
 // One CTA per tile of GROUPS x 32 pairs (pack_one_tile, pack_tile.cuh).
-template <int GROUPS, int ALIGN, bool NIB>
-__global__ void __launch_bounds__(kPackNT)
+// NFLAG: also write the N-presence flags (pack.cuh) and skip N-free tiles' N planes.
+// 4 CTAs/SM (128 registers): ptxas would otherwise take up to 180 and fit 2.
+template <int GROUPS, int ALIGN, bool NIB, bool NFLAG = false>
+__global__ void __launch_bounds__(kPackNT, 4)
 pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
                  size_t pitch, long long n, int m, uint32_t* __restrict__ planes,
-                 uint32_t* __restrict__ err_flag) {
+                 uint32_t* __restrict__ err_flag, uint32_t* __restrict__ nflags) {
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t sflag[2];
     if (threadIdx.x == 0) mbar_init(&bar, 1);
+    if (NFLAG && blockIdx.x == 0) {  // the all-zero N column image N-free groups read
+        uint32_t* zero = nflags + nflag_words(n);
+        for (int i = threadIdx.x; i < static_cast<int>(nzero_words(m)); i += kPackNT) zero[i] = 0u;
+    }
     __syncthreads();
-    const uint32_t err = pack_one_tile<ALIGN, kPackNT, NIB>(
+    const uint32_t err = pack_one_tile<ALIGN, kPackNT, NIB, NFLAG>(
         sm, &bar, 0, GROUPS, static_cast<long long>(blockIdx.x) * GROUPS, text, pattern, pitch, n, m,
-        planes);
+        planes, nflags, sflag);
     if (!NIB && err) atomicOr(err_flag, 1u);
 }
 
@@ -44,42 +51,70 @@ pack_direct_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__
     const long long g = (it / C) % ngroups;
     const int s = static_cast<int>(it / (C * ngroups));
     uint32_t sink[CH * 3];
-    uint32_t* dst = planes ? planes + plane_index(s, g, c * CH, 0, nblocks, mc) : sink;
+    uint32_t* dst = planes ? planes + lohi_index(s, g, c * CH, 0, nblocks, mc) : sink;
+    uint32_t* ndst = planes ? planes + nplane_index(s, g, c * CH, nblocks, mc) : sink + 2 * CH;
     const int stride = planes ? kPackGroups : 1;
-    const uint32_t err = produce_chunk(s == 0 ? text : pattern, pitch, g * 32, n, c, m, dst, stride);
+    const uint32_t err =
+        produce_chunk(s == 0 ? text : pattern, pitch, g * 32, n, c, m, dst, ndst, stride);
     if (err) atomicOr(err_flag, 1u);
 }
 
 }  // namespace
 
-template <int GROUPS, int ALIGN, bool NIB = false>
-static cudaError_t launch_tile(const uint8_t* text, const uint8_t* pattern, size_t pitch,
-                               long long n, int m, uint32_t* planes, uint32_t* err_flag,
-                               cudaStream_t s) {
-    const cudaError_t st = ensure_smem_attr<pack_tile_kernel<GROUPS, ALIGN, NIB>>(110 * 1024);
+template <int GROUPS, int ALIGN, bool NIB = false, bool NFLAG = false>
+static cudaError_t launch_tile_f(const uint8_t* text, const uint8_t* pattern, size_t pitch,
+                                 long long n, int m, uint32_t* planes, uint32_t* err_flag,
+                                 uint32_t* nflags, cudaStream_t s) {
+    const cudaError_t st = ensure_smem_attr<pack_tile_kernel<GROUPS, ALIGN, NIB, NFLAG>>(110 * 1024);
     if (st != cudaSuccess) return st;
     const long long ngroups = (n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + GROUPS - 1) / GROUPS);
-    pack_tile_kernel<GROUPS, ALIGN, NIB><<<grid, kPackNT, tile_smem(pitch, GROUPS), s>>>(
-        text, pattern, pitch, n, m, planes, err_flag);
+    pack_tile_kernel<GROUPS, ALIGN, NIB, NFLAG><<<grid, kPackNT, tile_smem(pitch, GROUPS), s>>>(
+        text, pattern, pitch, n, m, planes, err_flag, nflags);
     return cudaGetLastError();
 }
 
+template <int GROUPS, int ALIGN, bool NIB = false>
+static cudaError_t launch_tile(const uint8_t* text, const uint8_t* pattern, size_t pitch,
+                               long long n, int m, uint32_t* planes, uint32_t* err_flag,
+                               uint32_t* nflags, cudaStream_t s) {
+    return nflags ? launch_tile_f<GROUPS, ALIGN, NIB, true>(text, pattern, pitch, n, m, planes,
+                                                            err_flag, nflags, s)
+                  : launch_tile_f<GROUPS, ALIGN, NIB, false>(text, pattern, pitch, n, m, planes,
+                                                             err_flag, nullptr, s);
+}
+
+// The tile kernels can write N-presence flags when each thread owns at most
+// one (chunk, group, sequence) item.
+static bool tile_nflags_fit(size_t pitch, int m) {
+    const int groups = tile_groups(pitch);
+    return tile_smem(pitch, groups) <= 110 * 1024 && 2 * groups * ((m + CH - 1) / CH) <= kPackNT;
+}
+
+bool pack_writes_nflags(const FilterArgs& a) {
+    if (a.packed_text) return false;
+    if (a.dibits) return dibit_pack_fits(a.m);
+    if (a.nibbles) return tile_nflags_fit(nibble_pitch(a.m), a.m);
+    return a.pitch % 4 == 0 && tile_nflags_fit(a.pitch, a.m);
+}
+
 cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitch, long long n,
-                        int m, uint32_t* planes, uint32_t* err_flag, cudaStream_t s) {
+                        int m, uint32_t* planes, uint32_t* err_flag, cudaStream_t s,
+                        uint32_t* nflags) {
     if (n <= 0) return cudaSuccess;
     if (pitch % 4 != 0) return cudaErrorInvalidValue;
+    if (nflags && (!planes || !tile_nflags_fit(pitch, m))) return cudaErrorInvalidValue;
     const int groups = tile_groups(pitch);
     const size_t smem = tile_smem(pitch, groups);
     cudaError_t st;
     if (smem <= 110 * 1024) {
         const bool a16 = pitch % 16 == 0;
         if (groups == 8)
-            st = a16 ? launch_tile<8, 16>(text, pattern, pitch, n, m, planes, err_flag, s)
-                     : launch_tile<8, 4>(text, pattern, pitch, n, m, planes, err_flag, s);
+            st = a16 ? launch_tile<8, 16>(text, pattern, pitch, n, m, planes, err_flag, nflags, s)
+                     : launch_tile<8, 4>(text, pattern, pitch, n, m, planes, err_flag, nflags, s);
         else
-            st = a16 ? launch_tile<4, 16>(text, pattern, pitch, n, m, planes, err_flag, s)
-                     : launch_tile<4, 4>(text, pattern, pitch, n, m, planes, err_flag, s);
+            st = a16 ? launch_tile<4, 16>(text, pattern, pitch, n, m, planes, err_flag, nflags, s)
+                     : launch_tile<4, 4>(text, pattern, pitch, n, m, planes, err_flag, nflags, s);
     } else {
         const long long items = 2 * ((n + 31) / 32) * ((plane_cols(m) + CH - 1) / CH);
         pack_direct_kernel<<<static_cast<unsigned>((items + kPackNT - 1) / kPackNT), kPackNT, 0,
@@ -96,13 +131,15 @@ bool nibble_pack_fits(int m) {
 }
 
 cudaError_t launch_pack_nibbles(const uint8_t* text, const uint8_t* pattern, long long n, int m,
-                                uint32_t* planes, cudaStream_t s) {
+                                uint32_t* planes, cudaStream_t s, uint32_t* nflags) {
     if (n <= 0) return cudaSuccess;
     if (!nibble_pack_fits(m) || planes == nullptr) return cudaErrorInvalidValue;
     const size_t np = nibble_pitch(m);
-    const cudaError_t st = tile_groups(np) == 8
-                               ? launch_tile<8, 4, true>(text, pattern, np, n, m, planes, nullptr, s)
-                               : launch_tile<4, 4, true>(text, pattern, np, n, m, planes, nullptr, s);
+    if (nflags && !tile_nflags_fit(np, m)) return cudaErrorInvalidValue;
+    const cudaError_t st =
+        tile_groups(np) == 8
+            ? launch_tile<8, 4, true>(text, pattern, np, n, m, planes, nullptr, nflags, s)
+            : launch_tile<4, 4, true>(text, pattern, np, n, m, planes, nullptr, nflags, s);
     count_launch();
     return st;
 }
@@ -113,11 +150,14 @@ namespace {
 // One CTA per pair block (8 groups): a bulk copy per sequence brings the
 // block's dibit rows (and, for chunks with N, its N-plane rows) into shared
 // memory, then each thread gathers one (chunk, group, sequence) item.
-template <bool HAS_N>
+// nflags (optional): N-presence flags — without N rows every group is N-free
+// and its N planes are not stored; with N rows every group is flagged.
+template <bool HAS_N, bool SKIP_N = false>
 __global__ void __launch_bounds__(kPackNT)
 pack_dibit_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
                   const uint8_t* __restrict__ ntext, const uint8_t* __restrict__ npattern,
-                  long long n, int m, uint32_t* __restrict__ planes) {
+                  long long n, int m, uint32_t* __restrict__ planes,
+                  uint32_t* __restrict__ nflags) {
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ __align__(8) uint64_t bar;
     const int dp = static_cast<int>(dibit_pitch(m));
@@ -156,22 +196,31 @@ pack_dibit_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ 
     const int mc = plane_cols(m);
     const int C = (m + CH - 1) / CH;
     const int Cfull = m / CH;
+    if (nflags && threadIdx.x < 2 * kPackGroups)
+        nflags[nflag_index(threadIdx.x / kPackGroups,
+                           static_cast<long long>(blockIdx.x) * kPackGroups + threadIdx.x % kPackGroups,
+                           nblocks)] = HAS_N ? 1u : 0u;
+    if (nflags && blockIdx.x == 0) {  // the all-zero N column image N-free groups read
+        uint32_t* zero = nflags + nflag_words(n);
+        for (int i = threadIdx.x; i < static_cast<int>(nzero_words(m)); i += blockDim.x) zero[i] = 0u;
+    }
     for (int it = threadIdx.x; it < 2 * kPackGroups * C; it += blockDim.x) {
         const int c = it / (2 * kPackGroups);
         const int g = (it / 2) % kPackGroups;
         const int s = it % 2;
-        uint32_t* dst = planes + plane_index(s, static_cast<long long>(blockIdx.x) * kPackGroups + g,
-                                             c * CH, 0, nblocks, mc);
+        const long long gg = static_cast<long long>(blockIdx.x) * kPackGroups + g;
+        uint32_t* dst = planes + lohi_index(s, gg, c * CH, 0, nblocks, mc);
+        uint32_t* ndst = planes + nplane_index(s, gg, c * CH, nblocks, mc);
         const uint8_t* src = dib[s] + g * 32 * dp;
         const uint8_t* nsrc = nrow[s] + g * 32 * np;
         if (c < Cfull) {
-            gather_chunk_dib<false, 4, HAS_N>(src, dp, nsrc, np, c * CH, m, dst, kPackGroups);
+            gather_chunk_dib<false, 4, HAS_N, SKIP_N>(src, dp, nsrc, np, c * CH, m, dst, ndst, kPackGroups);
         } else {
             switch ((m - c * CH + 3) / 4) {
-                case 1: gather_chunk_dib<true, 1, HAS_N>(src, dp, nsrc, np, c * CH, m, dst, kPackGroups); break;
-                case 2: gather_chunk_dib<true, 2, HAS_N>(src, dp, nsrc, np, c * CH, m, dst, kPackGroups); break;
-                case 3: gather_chunk_dib<true, 3, HAS_N>(src, dp, nsrc, np, c * CH, m, dst, kPackGroups); break;
-                default: gather_chunk_dib<true, 4, HAS_N>(src, dp, nsrc, np, c * CH, m, dst, kPackGroups); break;
+                case 1: gather_chunk_dib<true, 1, HAS_N, SKIP_N>(src, dp, nsrc, np, c * CH, m, dst, ndst, kPackGroups); break;
+                case 2: gather_chunk_dib<true, 2, HAS_N, SKIP_N>(src, dp, nsrc, np, c * CH, m, dst, ndst, kPackGroups); break;
+                case 3: gather_chunk_dib<true, 3, HAS_N, SKIP_N>(src, dp, nsrc, np, c * CH, m, dst, ndst, kPackGroups); break;
+                default: gather_chunk_dib<true, 4, HAS_N, SKIP_N>(src, dp, nsrc, np, c * CH, m, dst, ndst, kPackGroups); break;
             }
         }
     }
@@ -187,7 +236,7 @@ bool dibit_pack_fits(int m) { return dibit_pack_smem(m) <= 200 * 1024; }
 
 cudaError_t launch_pack_dibits(const uint8_t* text, const uint8_t* pattern, const uint8_t* ntext,
                                const uint8_t* npattern, long long n, int m, uint32_t* planes,
-                               cudaStream_t s) {
+                               cudaStream_t s, uint32_t* nflags) {
     if (n <= 0) return cudaSuccess;
     if (!dibit_pack_fits(m) || planes == nullptr) return cudaErrorInvalidValue;
     const size_t smem = dibit_pack_smem(m);
@@ -197,12 +246,17 @@ cudaError_t launch_pack_dibits(const uint8_t* text, const uint8_t* pattern, cons
         st = ensure_smem_attr<pack_dibit_kernel<true>>(200 * 1024);
         if (st == cudaSuccess)
             pack_dibit_kernel<true><<<grid, kPackNT, smem, s>>>(text, pattern, ntext, npattern, n,
-                                                               m, planes);
+                                                               m, planes, nflags);
+    } else if (nflags != nullptr) {
+        st = ensure_smem_attr<pack_dibit_kernel<false, true>>(200 * 1024);
+        if (st == cudaSuccess)
+            pack_dibit_kernel<false, true><<<grid, kPackNT, smem, s>>>(text, pattern, nullptr,
+                                                                      nullptr, n, m, planes, nflags);
     } else {
         st = ensure_smem_attr<pack_dibit_kernel<false>>(200 * 1024);
         if (st == cudaSuccess)
             pack_dibit_kernel<false><<<grid, kPackNT, smem, s>>>(text, pattern, nullptr, nullptr,
-                                                                n, m, planes);
+                                                                n, m, planes, nullptr);
     }
     count_launch();
     return st != cudaSuccess ? st : cudaGetLastError();

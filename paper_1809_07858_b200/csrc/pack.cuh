@@ -11,10 +11,14 @@
 // 32-pair tiles out of shared memory (gather_chunk, phase_a.cuh) and the CTA
 // writes its planes back as one contiguous range per sequence:
 //
-//   planes[s][pair_block][col][plane][8 groups]      (uint32 words)
+//   planes [s][pair_block][col][lo, hi][8 groups]     (uint32 words)
+//   nplanes[s][pair_block][col][8 groups]              (after all lo/hi planes)
 //
 // so the filter kernel, whose thread owns one group and walks columns, reads
-// one fully used 32-byte sector per (column, plane) per 8 threads.
+// one fully used 32-byte sector per (column, plane) per 8 threads. The N
+// planes live in their own region so that N-free pair blocks (the usual case)
+// neither write nor read them: whole lines are skipped, not single sectors
+// inside lines that are written anyway (which saves no DRAM traffic).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -31,18 +35,46 @@ constexpr int kPackNT = 128;                    // threads per pack CTA
 // written or read).
 __host__ __device__ inline int plane_cols(int m) { return m; }
 
-// Words of plane storage for n pairs of length m (both sequences).
+// Words of plane storage for n pairs of length m (both sequences, lo/hi + N).
 inline size_t plane_words(long long n, int m) {
     const long long blocks = (n + kPackPairs - 1) / kPackPairs;
     return static_cast<size_t>(2 * blocks * plane_cols(m) * 3 * kPackGroups);
 }
 
-// Offset (in words) of plane word (s, group g, col, k); the group's 8-lane slot is g % 8.
-__host__ __device__ inline size_t plane_index(int s, long long g, int col, int k, long long nblocks,
-                                              int mc) {
+constexpr int kLhColWords = 2 * kPackGroups;  // lo/hi words per column of a pair block
+constexpr int kNColWords = kPackGroups;       // N words per column of a pair block
+
+// Offset (in words) of plane word (s, group g, col, k in {0 lo, 1 hi}); the
+// group's 8-lane slot is g % 8.
+__host__ __device__ inline size_t lohi_index(int s, long long g, int col, int k, long long nblocks,
+                                             int mc) {
     const long long blk = g / kPackGroups;
-    return ((static_cast<size_t>(s) * nblocks + blk) * mc + col) * (3 * kPackGroups) +
-           k * kPackGroups + (g % kPackGroups);
+    return ((static_cast<size_t>(s) * nblocks + blk) * mc + col) * kLhColWords + k * kPackGroups +
+           (g % kPackGroups);
+}
+
+// Offset (in words) of N-plane word (s, group g, col).
+__host__ __device__ inline size_t nplane_index(int s, long long g, int col, long long nblocks,
+                                               int mc) {
+    const long long blk = g / kPackGroups;
+    return static_cast<size_t>(2 * nblocks) * mc * kLhColWords +
+           ((static_cast<size_t>(s) * nblocks + blk) * mc + col) * kNColWords + (g % kPackGroups);
+}
+
+// N-presence flags, stored after the plane words: one uint32 per (sequence,
+// group), nonzero iff the N planes of that group were stored. A pack kernel
+// that writes flags stores the N planes of a tile's sequence only when one of
+// its records holds an N, and a search that reads flags points N-free groups
+// at an all-zero column image (after the flags, plane_cols(m) x 8 words) or,
+// for a warp of N-free groups, drops the N terms altogether.
+__host__ __device__ inline size_t nflag_words(long long n) {
+    return static_cast<size_t>(2 * ((n + kPackPairs - 1) / kPackPairs) * kPackGroups);
+}
+__host__ __device__ inline size_t nflag_index(int s, long long g, long long nblocks) {
+    return static_cast<size_t>(s) * nblocks * kPackGroups + g;
+}
+__host__ __device__ inline size_t nzero_words(int m) {
+    return static_cast<size_t>(plane_cols(m)) * kNColWords;
 }
 
 // Nibble records: the upload format of host-packed batches (host_pack.cpp).

@@ -123,15 +123,18 @@ pack_planes_kernel(const uint64_t* __restrict__ text, const uint64_t* __restrict
     }
     __syncthreads();
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
-    uint4* dst = reinterpret_cast<uint4*>(
-        planes + plane_index(s, static_cast<long long>(blockIdx.x) * kPackGroups, 0, 0, nblocks,
-                             plane_cols(m)));
-    constexpr int kRow = 3 * kPackGroups;  // 24 words per column in the planes layout
-    const int chunks = m * kRow / 4;
-    for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
-        const int col = __umulhi(static_cast<uint32_t>(4 * c), 0x0AAAAAABu);  // (4c) / 24
-        const uint32_t* src_w = out + col * kOut + (4 * c - col * kRow);
+    const long long g0 = static_cast<long long>(blockIdx.x) * kPackGroups;
+    // lo/hi region: 16 words per column (image words 0..15), then the N region:
+    // 8 words per column (image words 16..23)
+    uint4* dst = reinterpret_cast<uint4*>(planes + lohi_index(s, g0, 0, 0, nblocks, plane_cols(m)));
+    for (int c = threadIdx.x; c < m * kLhColWords / 4; c += blockDim.x) {
+        const uint32_t* src_w = out + (c >> 2) * kOut + 4 * (c & 3);
         dst[c] = make_uint4(src_w[0], src_w[1], src_w[2], src_w[3]);
+    }
+    uint4* ndst = reinterpret_cast<uint4*>(planes + nplane_index(s, g0, 0, nblocks, plane_cols(m)));
+    for (int c = threadIdx.x; c < m * kNColWords / 4; c += blockDim.x) {
+        const uint32_t* src_w = out + (c >> 1) * kOut + kLhColWords + 4 * (c & 1);
+        ndst[c] = make_uint4(src_w[0], src_w[1], src_w[2], src_w[3]);
     }
 }
 
@@ -164,7 +167,9 @@ pack_planes_direct_kernel(const uint64_t* __restrict__ text, const uint64_t* __r
             const uint32_t x = live ? __ldg(row + k * 2 * w64 + j) : 0u;
             const uint32_t col_word = transpose32(x);
             const int col = 32 * j + lane;
-            if (col < m) planes[plane_index(s, g, col, k, nblocks, mc)] = col_word;
+            if (col < m)
+                planes[k < 2 ? lohi_index(s, g, col, k, nblocks, mc)
+                             : nplane_index(s, g, col, nblocks, mc)] = col_word;
         }
     }
 }

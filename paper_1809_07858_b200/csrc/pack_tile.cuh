@@ -59,23 +59,24 @@ __host__ __device__ inline size_t seq_stride(size_t pitch, int groups) {
 inline size_t tile_smem(size_t pitch, int groups) { return 2 * seq_stride(pitch, groups) + 128; }
 inline int tile_groups(size_t pitch) { return pitch <= 128 ? 8 : 4; }
 
-template <bool EDGE, int ALIGN, bool NIB = false>
+template <bool EDGE, int ALIGN, bool NIB = false, bool DEFER_N = false>
 __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size_t pitch, int col0,
-                                               int m, uint32_t* dst, int stride) {
+                                               int m, uint32_t* dst, uint32_t* ndst, int stride,
+                                               uint32_t* nout = nullptr) {
     if constexpr (NIB) {
         switch (ncg) {
-            case 1: gather_chunk_nib<EDGE, 1>(src, pitch, col0, m, dst, stride); break;
-            case 2: gather_chunk_nib<EDGE, 2>(src, pitch, col0, m, dst, stride); break;
-            case 3: gather_chunk_nib<EDGE, 3>(src, pitch, col0, m, dst, stride); break;
-            default: gather_chunk_nib<EDGE, 4>(src, pitch, col0, m, dst, stride); break;
+            case 1: gather_chunk_nib<EDGE, 1, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout); break;
+            case 2: gather_chunk_nib<EDGE, 2, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout); break;
+            case 3: gather_chunk_nib<EDGE, 3, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout); break;
+            default: gather_chunk_nib<EDGE, 4, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout); break;
         }
         return 0u;
     }
     switch (ncg) {
-        case 1: return gather_chunk<EDGE, false, 1, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
-        case 2: return gather_chunk<EDGE, false, 2, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
-        case 3: return gather_chunk<EDGE, false, 3, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
-        default: return gather_chunk<EDGE, false, 4, ALIGN>(src, pitch, 0, 32, col0, m, dst, stride);
+        case 1: return gather_chunk<EDGE, false, 1, ALIGN, DEFER_N>(src, pitch, 0, 32, col0, m, dst, ndst, stride, nout);
+        case 2: return gather_chunk<EDGE, false, 2, ALIGN, DEFER_N>(src, pitch, 0, 32, col0, m, dst, ndst, stride, nout);
+        case 3: return gather_chunk<EDGE, false, 3, ALIGN, DEFER_N>(src, pitch, 0, 32, col0, m, dst, ndst, stride, nout);
+        default: return gather_chunk<EDGE, false, 4, ALIGN, DEFER_N>(src, pitch, 0, 32, col0, m, dst, ndst, stride, nout);
     }
 }
 
@@ -84,12 +85,18 @@ __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size
 // bar: an initialised mbarrier; parity: its current phase (flipped on return
 // by the caller). Returns nonzero on an illegal byte. NIB: the records are
 // nibble records (pack.cuh; pitch = nibble_pitch(m)), validated by the host.
-template <int ALIGN, int NT, bool NIB = false>
+// NFLAG: write the tile's N-presence flags (pack.cuh) and store a sequence's
+// N planes only when one of the tile's records of that sequence holds an N;
+// needs one item per thread (2 * GROUPS * ceil(m/16) <= NT) and sflag, 2 words
+// of shared memory.
+template <int ALIGN, int NT, bool NIB = false, bool NFLAG = false>
 __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, uint32_t parity,
                                                   int GROUPS, long long g0,
                                                   const uint8_t* __restrict__ text,
                                                   const uint8_t* __restrict__ pattern, size_t pitch,
-                                                  long long n, int m, uint32_t* __restrict__ planes) {
+                                                  long long n, int m, uint32_t* __restrict__ planes,
+                                                  uint32_t* __restrict__ nflags = nullptr,
+                                                  uint32_t* sflag = nullptr) {
     const long long row0 = g0 * 32;
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
     const int rows = static_cast<int>(n - row0 < 32 * GROUPS ? n - row0 : 32 * GROUPS);
@@ -108,6 +115,7 @@ __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, ui
         for (int g = 0; g < GROUPS; ++g) total += 2u * static_cast<uint32_t>(tma_bytes(g));
         mbar_expect_tx(bar, total);
     }
+    if (NFLAG && threadIdx.x < 2) sflag[threadIdx.x] = 0u;
     __syncthreads();  // expect_tx before any complete_tx; previous tile's readers done
     if (threadIdx.x < 2 * GROUPS) {
         const int sq = threadIdx.x / GROUPS, g = threadIdx.x % GROUPS;
@@ -144,21 +152,50 @@ __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, ui
     const int Cfull = m / CH;  // chunks entirely inside [0, m)
     uint32_t err = 0u;
     uint32_t sink[CH * 3];
+    uint32_t nw[CH];        // NFLAG: this thread's item's N-plane words
+    uint32_t* ndst = nullptr;
+    int nseq = 0, ncols = 0;
     for (int it = threadIdx.x; it < 2 * GROUPS * C; it += NT) {
         const int c = it / (2 * GROUPS);
         const int g = (it / 2) % GROUPS;
         const int sq = it % 2;
-        uint32_t* dst = planes ? planes + plane_index(sq, g0 + g, c * CH, 0, nblocks, mc) : sink;
+        uint32_t* dst = planes ? planes + lohi_index(sq, g0 + g, c * CH, 0, nblocks, mc) : sink;
+        uint32_t* nd = planes ? planes + nplane_index(sq, g0 + g, c * CH, nblocks, mc) : sink + 2 * CH;
         const int stride = planes ? kPackGroups : 1;
+        if constexpr (NFLAG) {  // an edge chunk's gather fills only its first 4*ncg words
+#pragma unroll
+            for (int col = 0; col < CH; ++col) nw[col] = 0u;
+        }
         if (c < Cfull) {
             if constexpr (NIB)
-                gather_chunk_nib<false, 4>(rec(sq, g), pitch, c * CH, m, dst, stride);
+                gather_chunk_nib<false, 4, NFLAG>(rec(sq, g), pitch, c * CH, m, dst, nd, stride, nw);
             else
-                err |= gather_chunk<false, false, 4, ALIGN>(rec(sq, g), pitch, 0, 32, c * CH, m,
-                                                             dst, stride);
+                err |= gather_chunk<false, false, 4, ALIGN, NFLAG>(rec(sq, g), pitch, 0, 32, c * CH,
+                                                                    m, dst, nd, stride, nw);
         } else {
-            err |= gather_ncg<true, ALIGN, NIB>((m - c * CH + 3) / 4, rec(sq, g), pitch, c * CH, m,
-                                                dst, stride);
+            err |= gather_ncg<true, ALIGN, NIB, NFLAG>((m - c * CH + 3) / 4, rec(sq, g), pitch,
+                                                       c * CH, m, dst, nd, stride, nw);
+        }
+        if constexpr (NFLAG) {
+            uint32_t any = 0u;
+#pragma unroll
+            for (int col = 0; col < CH; ++col) any |= nw[col];
+            if (any) sflag[sq] = 1u;
+            ndst = nd;
+            nseq = sq;
+            ncols = c < Cfull ? CH : m - c * CH;
+        }
+    }
+    if constexpr (NFLAG) {
+        __syncthreads();
+        if (ndst != nullptr && sflag[nseq]) {
+#pragma unroll
+            for (int col = 0; col < CH; ++col)
+                if (col < ncols) ndst[col * kNColWords] = nw[col];
+        }
+        if (threadIdx.x < 2 * GROUPS) {
+            const int sq = threadIdx.x / GROUPS, g = threadIdx.x % GROUPS;
+            nflags[nflag_index(sq, g0 + g, nblocks)] = sflag[sq];
         }
     }
     return err;

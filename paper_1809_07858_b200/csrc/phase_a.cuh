@@ -49,8 +49,8 @@ __device__ __forceinline__ uint4 load_row16(const uint8_t* p) {
     }
 }
 
-// Gather columns [col0, col0 + 4*NCG) of rows [row0, row0+32) into plane words.
-// dst[(col*3 + k) * dstride], k = 0 lo, 1 hi, 2 N. Returns nonzero on any
+// Gather columns [col0, col0 + 4*NCG) of rows [row0, row0+32) into plane words:
+// dst[(col*2 + k) * dstride], k = 0 lo, 1 hi, and ndst[col * dstride] (N). Returns nonzero on any
 // illegal byte. EDGE: the chunk straddles m (bytes at columns >= m are
 // ignored; only columns < m are stored). NCG: column groups of 4 processed
 // (fewer than 4 only for the chunk straddling m). ALIGN: row alignment (16/4).
@@ -59,10 +59,16 @@ __device__ __forceinline__ uint4 load_row16(const uint8_t* p) {
 // accumulator by a per-plane shift (left for i >= k, right otherwise) — a
 // multiply or a high multiply, so the shifts issue on the FMA pipe and the
 // ALU pipe only sees the masked ORs.
-template <bool EDGE, bool CHECK_ROWS = true, int NCG = 4, int ALIGN = 16>
+//
+// DEFER_N: the N-plane words are not stored but returned in nout[0..4*NCG)
+// (0 for columns >= m), for pack kernels that write them only for groups that
+// hold an N (pack.cuh, N-presence flags).
+template <bool EDGE, bool CHECK_ROWS = true, int NCG = 4, int ALIGN = 16, bool DEFER_N = false>
 __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq, size_t pitch,
                                                  long long row0, long long n, int col0, int m,
-                                                 uint32_t* __restrict__ dst, int dstride) {
+                                                 uint32_t* __restrict__ dst,
+                                                 uint32_t* __restrict__ ndst, int dstride,
+                                                 uint32_t* __restrict__ nout = nullptr) {
     uint32_t O[NCG][3][4];  // [column group][plane][column in group] -> column words
 #pragma unroll
     for (int cg = 0; cg < NCG; ++cg)
@@ -140,9 +146,11 @@ __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int col = 4 * cg + q;
+            if constexpr (DEFER_N) nout[col] = O[cg][2][q];  // columns >= m read as 'A': 0
             if (EDGE && col0 + col >= m) continue;  // never read: columns >= m are N
-#pragma unroll
-            for (int k = 0; k < 3; ++k) dst[(col * 3 + k) * dstride] = O[cg][k][q];
+            dst[(col * 2 + 0) * dstride] = O[cg][0][q];
+            dst[(col * 2 + 1) * dstride] = O[cg][1][q];
+            if constexpr (!DEFER_N) ndst[col * dstride] = O[cg][2][q];
         }
     return err;
 }
@@ -152,10 +160,11 @@ __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq
 // is word cg/2, low nibbles for even cg, high nibbles for odd cg, so ASCII bit
 // k of column 4cg+q sits at bit 8q + 4(cg&1) + k of the word and reaches bit
 // 8q+i of the plane-k accumulator by one shift, as in gather_chunk.
-template <bool EDGE, int NCG>
+template <bool EDGE, int NCG, bool DEFER_N = false>
 __device__ __forceinline__ void gather_chunk_nib(const uint8_t* __restrict__ seq, size_t pitch,
                                                  int col0, int m, uint32_t* __restrict__ dst,
-                                                 int dstride) {
+                                                 uint32_t* __restrict__ ndst, int dstride,
+                                                 uint32_t* __restrict__ nout = nullptr) {
     constexpr int NW = (NCG + 1) / 2;
     uint32_t O[NCG][3][4];
 #pragma unroll
@@ -204,9 +213,11 @@ __device__ __forceinline__ void gather_chunk_nib(const uint8_t* __restrict__ seq
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int col = 4 * cg + q;
+            if constexpr (DEFER_N) nout[col] = O[cg][2][q];  // columns >= m are zero nibbles
             if (EDGE && col0 + col >= m) continue;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) dst[(col * 3 + k) * dstride] = O[cg][k][q];
+            dst[(col * 2 + 0) * dstride] = O[cg][0][q];
+            dst[(col * 2 + 1) * dstride] = O[cg][1][q];
+            if constexpr (!DEFER_N) ndst[col * dstride] = O[cg][2][q];
         }
 }
 
@@ -216,11 +227,14 @@ __device__ __forceinline__ void gather_chunk_nib(const uint8_t* __restrict__ seq
 // reaches bit 8q+i of the accumulator by one shift. The N plane comes from the
 // optional N-plane rows (bit c = column c); without them every column is
 // N-free.
-template <bool EDGE, int NCG, bool HAS_N>
+// SKIP_N (only without HAS_N): the all-zero N plane is not stored (the
+// group's N-presence flag says so, pack.cuh).
+template <bool EDGE, int NCG, bool HAS_N, bool SKIP_N = false>
 __device__ __forceinline__ void gather_chunk_dib(const uint8_t* __restrict__ seq, size_t pitch,
                                                  const uint8_t* __restrict__ nseq, size_t npitch,
                                                  int col0, int m, uint32_t* __restrict__ dst,
-                                                 int dstride) {
+                                                 uint32_t* __restrict__ ndst, int dstride) {
+    static_assert(!(HAS_N && SKIP_N), "N planes with N data are always stored");
     uint32_t O[NCG][3][4];
 #pragma unroll
     for (int cg = 0; cg < NCG; ++cg)
@@ -276,18 +290,20 @@ __device__ __forceinline__ void gather_chunk_dib(const uint8_t* __restrict__ seq
         for (int q = 0; q < 4; ++q) {
             const int col = 4 * cg + q;
             if (EDGE && col0 + col >= m) continue;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) dst[(col * 3 + k) * dstride] = O[cg][k][q];
+            dst[(col * 2 + 0) * dstride] = O[cg][0][q];
+            dst[(col * 2 + 1) * dstride] = O[cg][1][q];
+            if constexpr (!SKIP_N) ndst[col * dstride] = O[cg][2][q];
         }
 }
 
 // A chunk entirely outside [0, m): every column is N.
-__device__ __forceinline__ void fill_oob_chunk(uint32_t* __restrict__ dst, int dstride) {
+__device__ __forceinline__ void fill_oob_chunk(uint32_t* __restrict__ dst,
+                                               uint32_t* __restrict__ ndst, int dstride) {
 #pragma unroll
     for (int col = 0; col < CH; ++col) {
-        dst[(col * 3 + 0) * dstride] = 0u;
-        dst[(col * 3 + 1) * dstride] = 0u;
-        dst[(col * 3 + 2) * dstride] = ~0u;
+        dst[(col * 2 + 0) * dstride] = 0u;
+        dst[(col * 2 + 1) * dstride] = 0u;
+        ndst[col * dstride] = ~0u;
     }
 }
 
@@ -295,15 +311,16 @@ __device__ __forceinline__ void fill_oob_chunk(uint32_t* __restrict__ dst, int d
 // 4-byte aligned.
 __device__ __forceinline__ uint32_t produce_chunk(const uint8_t* __restrict__ seq, size_t pitch,
                                                   long long row0, long long n, int chunk, int m,
-                                                  uint32_t* __restrict__ dst, int dstride) {
+                                                  uint32_t* __restrict__ dst,
+                                                  uint32_t* __restrict__ ndst, int dstride) {
     const int col0 = chunk * CH;
     if (chunk < 0 || col0 >= m) {
-        fill_oob_chunk(dst, dstride);
+        fill_oob_chunk(dst, ndst, dstride);
         return 0u;
     }
     if (col0 + CH <= m)
-        return gather_chunk<false, true, 4, 4>(seq, pitch, row0, n, col0, m, dst, dstride);
-    return gather_chunk<true, true, 4, 4>(seq, pitch, row0, n, col0, m, dst, dstride);
+        return gather_chunk<false, true, 4, 4>(seq, pitch, row0, n, col0, m, dst, ndst, dstride);
+    return gather_chunk<true, true, 4, 4>(seq, pitch, row0, n, col0, m, dst, ndst, dstride);
 }
 
 }  // namespace sb

@@ -96,8 +96,10 @@ struct CandW {
 };
 
 template <int W, bool CHECK>
-__device__ __forceinline__ void wsearch_block(const uint32_t* __restrict__ tbase, int tcol0,
-                                              const uint32_t* __restrict__ pbase, int pcol0,
+__device__ __forceinline__ void wsearch_block(const uint32_t* __restrict__ tbase,
+                                              const uint32_t* __restrict__ tnbase, int tcol0,
+                                              const uint32_t* __restrict__ pbase,
+                                              const uint32_t* __restrict__ pnbase, int pcol0,
                                               int m, int E, CandW<W> (&best)[4]) {
     constexpr int B = 4;
     constexpr int X = B + W - 1;
@@ -105,10 +107,10 @@ __device__ __forceinline__ void wsearch_block(const uint32_t* __restrict__ tbase
     constexpr int NO = WPlanes<W>::NO;
     uint32_t T[X][3];
 #pragma unroll
-    for (int x = 0; x < X; ++x) load_rel<CHECK, true>(tbase, x, tcol0, m, T[x]);
+    for (int x = 0; x < X; ++x) load_rel<CHECK, true>(tbase, tnbase, x, tcol0, m, T[x]);
     uint32_t P[X][3];
 #pragma unroll
-    for (int x = 0; x < X; ++x) load_rel<CHECK, true>(pbase, x, pcol0, m, P[x]);
+    for (int x = 0; x < X; ++x) load_rel<CHECK, true>(pbase, pnbase, x, pcol0, m, P[x]);
     auto step = [&](const int rot, bool first) {
         uint32_t sv[X];
 #pragma unroll
@@ -146,7 +148,7 @@ __device__ __forceinline__ void wsearch_block(const uint32_t* __restrict__ tbase
         for (int u = 0; u < X; ++u) {
             const int di = d0 + u;
             if (di > 2 * E) break;
-            load_rel<CHECK, true>(pbase, di + X - 1, pcol0, m, P[u]);
+            load_rel<CHECK, true>(pbase, pnbase, di + X - 1, pcol0, m, P[u]);
             step((1 + u) % X, false);
         }
     }
@@ -179,14 +181,15 @@ __device__ __forceinline__ void wsearch_group(const uint32_t* __restrict__ plane
                                               uint32_t* __restrict__ outplanes) {
     constexpr int B = 4;
     constexpr int X = B + W - 1;
-    constexpr int COLW = 3 * kPackGroups;
     const long long row0 = g * 32;
     if (row0 >= n) return;
     const long long ngroups = (n + 31) / 32;
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
     const int mc = plane_cols(m);
-    const uint32_t* const tb = planes + plane_index(0, g, 0, 0, nblocks, mc);
-    const uint32_t* const pb = planes + plane_index(1, g, 0, 0, nblocks, mc);
+    const uint32_t* const tb = planes + lohi_index(0, g, 0, 0, nblocks, mc);
+    const uint32_t* const pb = planes + lohi_index(1, g, 0, 0, nblocks, mc);
+    const uint32_t* const tnb = planes + nplane_index(0, g, 0, nblocks, mc);
+    const uint32_t* const pnb = planes + nplane_index(1, g, 0, nblocks, mc);
     uint32_t S[W - 1];
 #pragma unroll
     for (int i = 0; i < W - 1; ++i) S[i] = ~0u;  // bitvector bv(m, true) (shouji.cpp:52)
@@ -199,13 +202,15 @@ __device__ __forceinline__ void wsearch_group(const uint32_t* __restrict__ plane
         const int j0 = blk * B;
         const int pcol0 = j0 - E;
         const bool interior = pcol0 >= 0 && j0 + X + E <= m;
-        const uint32_t* tbase = tb + static_cast<long long>(j0) * COLW;
-        const uint32_t* pbase = pb + static_cast<long long>(pcol0) * COLW;
+        const uint32_t* tbase = tb + static_cast<long long>(j0) * kLhColWords;
+        const uint32_t* pbase = pb + static_cast<long long>(pcol0) * kLhColWords;
+        const uint32_t* tnbase = tnb + static_cast<long long>(j0) * kNColWords;
+        const uint32_t* pnbase = pnb + static_cast<long long>(pcol0) * kNColWords;
         CandW<W> best[B];
         if (interior)
-            wsearch_block<W, false>(tbase, j0, pbase, pcol0, m, E, best);
+            wsearch_block<W, false>(tbase, tnbase, j0, pbase, pnbase, pcol0, m, E, best);
         else
-            wsearch_block<W, true>(tbase, j0, pbase, pcol0, m, E, best);
+            wsearch_block<W, true>(tbase, tnbase, j0, pbase, pnbase, pcol0, m, E, best);
         uint32_t outs[B];
 #pragma unroll
         for (int b = 0; b < B; ++b) {

@@ -463,3 +463,28 @@ def test_width4_long_records(gpu, oracle, m):
         a, est = check_batch(gpu, oracle, t, p, e)
         if m >= 1000:
             assert est.max() > 255  # the counter really goes past 8 planes
+
+
+@pytest.mark.parametrize("m", [17, 64, 100, 128, 129, 150, 250, 256, 300])
+def test_sparse_n_groups(gpu, oracle, m):
+    """N-presence flags (pack.cuh): N-free groups skip their N planes and a warp of
+    N-free groups runs the N-free search. N here sits in a few groups only — text-only,
+    pattern-only, both, in the first/last column and in the ragged last group — so one
+    launch mixes N-free warps, mixed warps and N warps."""
+    rng = np.random.default_rng(4242 + m)
+    n = 40_000 + 13
+    acgt = np.frombuffer(b"ACGT", np.uint8)
+    t = acgt[rng.integers(0, 4, size=(n, m))]
+    p = t.copy()
+    mask = rng.random(p.shape) < 0.05
+    p[mask] = acgt[rng.integers(0, 4, size=int(mask.sum()))]
+    for i in range(0, n, 5):
+        s = int(rng.integers(1, 3))
+        p[i, m // 3:] = np.roll(p[i, m // 3:], s)
+    t[5, 0] = ord("N")                 # group 0, text, first column
+    p[40, m - 1] = ord("N")            # group 1, pattern, last column
+    t[1100, m // 2] = p[1100, m // 2] = ord("N")  # same column in both
+    p[2 * 1024 + 77, 3 % m] = ord("N")   # one group in the third warp
+    t[n - 1, m // 2] = ord("N")        # the ragged last group
+    for e in sorted({0, 3, 5, 9, 13, min(m - 1, 25)}):
+        check_batch(gpu, oracle, t, p, e)
