@@ -14,7 +14,7 @@ namespace {
 // One CTA per tile of GROUPS x 32 pairs (pack_one_tile, pack_tile.cuh).
 // NFLAG: also write the N-presence flags (pack.cuh) and skip N-free tiles' N planes.
 // 4 CTAs/SM (128 registers): ptxas would otherwise take up to 180 and fit 2.
-template <int GROUPS, int ALIGN, bool NIB, bool NFLAG = false>
+template <int GROUPS, int PM, bool NIB, bool NFLAG = false>
 __global__ void __launch_bounds__(kPackNT, 4)
 pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
                  size_t pitch, long long n, int m, uint32_t* __restrict__ planes,
@@ -28,7 +28,7 @@ pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ p
         for (int i = threadIdx.x; i < static_cast<int>(nzero_words(m)); i += kPackNT) zero[i] = 0u;
     }
     __syncthreads();
-    const uint32_t err = pack_one_tile<ALIGN, kPackNT, NIB, NFLAG>(
+    const uint32_t err = pack_one_tile<PM, kPackNT, NIB, NFLAG>(
         sm, &bar, 0, GROUPS, static_cast<long long>(blockIdx.x) * GROUPS, text, pattern, pitch, n, m,
         planes, nflags, sflag);
     if (!NIB && err) atomicOr(err_flag, 1u);
@@ -61,26 +61,26 @@ pack_direct_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__
 
 }  // namespace
 
-template <int GROUPS, int ALIGN, bool NIB = false, bool NFLAG = false>
+template <int GROUPS, int PM, bool NIB = false, bool NFLAG = false>
 static cudaError_t launch_tile_f(const uint8_t* text, const uint8_t* pattern, size_t pitch,
                                  long long n, int m, uint32_t* planes, uint32_t* err_flag,
                                  uint32_t* nflags, cudaStream_t s) {
-    const cudaError_t st = ensure_smem_attr<pack_tile_kernel<GROUPS, ALIGN, NIB, NFLAG>>(110 * 1024);
+    const cudaError_t st = ensure_smem_attr<pack_tile_kernel<GROUPS, PM, NIB, NFLAG>>(110 * 1024);
     if (st != cudaSuccess) return st;
     const long long ngroups = (n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + GROUPS - 1) / GROUPS);
-    pack_tile_kernel<GROUPS, ALIGN, NIB, NFLAG><<<grid, kPackNT, tile_smem(pitch, GROUPS), s>>>(
+    pack_tile_kernel<GROUPS, PM, NIB, NFLAG><<<grid, kPackNT, tile_smem(pitch, GROUPS), s>>>(
         text, pattern, pitch, n, m, planes, err_flag, nflags);
     return cudaGetLastError();
 }
 
-template <int GROUPS, int ALIGN, bool NIB = false>
+template <int GROUPS, int PM, bool NIB = false>
 static cudaError_t launch_tile(const uint8_t* text, const uint8_t* pattern, size_t pitch,
                                long long n, int m, uint32_t* planes, uint32_t* err_flag,
                                uint32_t* nflags, cudaStream_t s) {
-    return nflags ? launch_tile_f<GROUPS, ALIGN, NIB, true>(text, pattern, pitch, n, m, planes,
+    return nflags ? launch_tile_f<GROUPS, PM, NIB, true>(text, pattern, pitch, n, m, planes,
                                                             err_flag, nflags, s)
-                  : launch_tile_f<GROUPS, ALIGN, NIB, false>(text, pattern, pitch, n, m, planes,
+                  : launch_tile_f<GROUPS, PM, NIB, false>(text, pattern, pitch, n, m, planes,
                                                              err_flag, nullptr, s);
 }
 
@@ -108,13 +108,23 @@ cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitc
     const size_t smem = tile_smem(pitch, groups);
     cudaError_t st;
     if (smem <= 110 * 1024) {
-        const bool a16 = pitch % 16 == 0;
-        if (groups == 8)
-            st = a16 ? launch_tile<8, 16>(text, pattern, pitch, n, m, planes, err_flag, nflags, s)
-                     : launch_tile<8, 4>(text, pattern, pitch, n, m, planes, err_flag, nflags, s);
-        else
-            st = a16 ? launch_tile<4, 16>(text, pattern, pitch, n, m, planes, err_flag, nflags, s)
-                     : launch_tile<4, 4>(text, pattern, pitch, n, m, planes, err_flag, nflags, s);
+        // row i of a group starts (i * pm) % 4 words past a 16-byte boundary
+        const int pm = static_cast<int>((pitch / 4) % 4);
+        if (groups == 8) {
+            switch (pm) {
+                case 0: st = launch_tile<8, 0>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+                case 1: st = launch_tile<8, 1>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+                case 2: st = launch_tile<8, 2>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+                default: st = launch_tile<8, 3>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+            }
+        } else {
+            switch (pm) {
+                case 0: st = launch_tile<4, 0>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+                case 1: st = launch_tile<4, 1>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+                case 2: st = launch_tile<4, 2>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+                default: st = launch_tile<4, 3>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+            }
+        }
     } else {
         const long long items = 2 * ((n + 31) / 32) * ((plane_cols(m) + CH - 1) / CH);
         pack_direct_kernel<<<static_cast<unsigned>((items + kPackNT - 1) / kPackNT), kPackNT, 0,
@@ -138,8 +148,8 @@ cudaError_t launch_pack_nibbles(const uint8_t* text, const uint8_t* pattern, lon
     if (nflags && !tile_nflags_fit(np, m)) return cudaErrorInvalidValue;
     const cudaError_t st =
         tile_groups(np) == 8
-            ? launch_tile<8, 4, true>(text, pattern, np, n, m, planes, nullptr, nflags, s)
-            : launch_tile<4, 4, true>(text, pattern, np, n, m, planes, nullptr, nflags, s);
+            ? launch_tile<8, 0, true>(text, pattern, np, n, m, planes, nullptr, nflags, s)
+            : launch_tile<4, 0, true>(text, pattern, np, n, m, planes, nullptr, nflags, s);
     count_launch();
     return st;
 }

@@ -59,7 +59,7 @@ __host__ __device__ inline size_t seq_stride(size_t pitch, int groups) {
 inline size_t tile_smem(size_t pitch, int groups) { return 2 * seq_stride(pitch, groups) + 128; }
 inline int tile_groups(size_t pitch) { return pitch <= 128 ? 8 : 4; }
 
-template <bool EDGE, int ALIGN, bool NIB = false, bool DEFER_N = false>
+template <bool EDGE, int PM, bool NIB = false, bool DEFER_N = false>
 __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size_t pitch, int col0,
                                                int m, uint32_t* dst, uint32_t* ndst, int stride,
                                                uint32_t* nout = nullptr) {
@@ -73,10 +73,10 @@ __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size
         return 0u;
     }
     switch (ncg) {
-        case 1: return gather_chunk<EDGE, false, 1, ALIGN, DEFER_N>(src, pitch, 0, 32, col0, m, dst, ndst, stride, nout);
-        case 2: return gather_chunk<EDGE, false, 2, ALIGN, DEFER_N>(src, pitch, 0, 32, col0, m, dst, ndst, stride, nout);
-        case 3: return gather_chunk<EDGE, false, 3, ALIGN, DEFER_N>(src, pitch, 0, 32, col0, m, dst, ndst, stride, nout);
-        default: return gather_chunk<EDGE, false, 4, ALIGN, DEFER_N>(src, pitch, 0, 32, col0, m, dst, ndst, stride, nout);
+        case 1: return gather_chunk_smem<EDGE, 1, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+        case 2: return gather_chunk_smem<EDGE, 2, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+        case 3: return gather_chunk_smem<EDGE, 3, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+        default: return gather_chunk_smem<EDGE, 4, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
     }
 }
 
@@ -89,7 +89,7 @@ __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size
 // N planes only when one of the tile's records of that sequence holds an N;
 // needs one item per thread (2 * GROUPS * ceil(m/16) <= NT) and sflag, 2 words
 // of shared memory.
-template <int ALIGN, int NT, bool NIB = false, bool NFLAG = false>
+template <int PM, int NT, bool NIB = false, bool NFLAG = false>
 __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, uint32_t parity,
                                                   int GROUPS, long long g0,
                                                   const uint8_t* __restrict__ text,
@@ -170,10 +170,10 @@ __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, ui
             if constexpr (NIB)
                 gather_chunk_nib<false, 4, NFLAG>(rec(sq, g), pitch, c * CH, m, dst, nd, stride, nw);
             else
-                err |= gather_chunk<false, false, 4, ALIGN, NFLAG>(rec(sq, g), pitch, 0, 32, c * CH,
-                                                                    m, dst, nd, stride, nw);
+                err |= gather_chunk_smem<false, 4, PM, NFLAG>(rec(sq, g), pitch, c * CH, m, dst, nd,
+                                                                stride, nw);
         } else {
-            err |= gather_ncg<true, ALIGN, NIB, NFLAG>((m - c * CH + 3) / 4, rec(sq, g), pitch,
+            err |= gather_ncg<true, PM, NIB, NFLAG>((m - c * CH + 3) / 4, rec(sq, g), pitch,
                                                        c * CH, m, dst, nd, stride, nw);
         }
         if constexpr (NFLAG) {

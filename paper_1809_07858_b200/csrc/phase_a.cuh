@@ -155,6 +155,123 @@ __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq
     return err;
 }
 
+// 8x8 bit transpose inside every byte lane of w[0..7]: afterwards bit i of
+// byte q of w[k] is bit k of byte q of the input w[i]. Three delta-swap stages
+// (4-, 2-, 1-bit blocks); each pair exchange is two shifts, issued as a
+// multiply / high multiply on the FMA pipe, and two LOP3 selects:
+//   a' = (a & lo) | (b << S & ~lo),   b' = (a >> S & lo) | (b & ~lo).
+// No bit crosses a byte: the masks keep only bits that moved inside it.
+__device__ __forceinline__ void transpose8_bytes(uint32_t (&w)[8]) {
+    auto xchg = [](uint32_t& a, uint32_t& b, uint32_t lo, int s) {
+        const uint32_t x = b * (1u << s);               // b << s
+        const uint32_t y = __umulhi(a, 1u << (32 - s));  // a >> s
+        a = lop3<0xE4>(a, x, lo);                       // lo ? a : x
+        b = lop3<0xE4>(y, b, lo);                       // lo ? y : b
+    };
+#pragma unroll
+    for (int i = 0; i < 4; ++i) xchg(w[i], w[i + 4], 0x0F0F0F0Fu, 4);
+    xchg(w[0], w[2], 0x33333333u, 2);
+    xchg(w[1], w[3], 0x33333333u, 2);
+    xchg(w[4], w[6], 0x33333333u, 2);
+    xchg(w[5], w[7], 0x33333333u, 2);
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) xchg(w[i], w[i + 1], 0x55555555u, 1);
+}
+
+// Bytes [4*mis, 4*mis + 4*NCG) of two 16-byte-aligned shared-memory chunks at
+// p - 4*mis, i.e. the NCG words at p (mis = p's word offset past a 16-byte
+// boundary, a compile-time constant once the caller's row loop is unrolled).
+// One LDS.128 (two when the words straddle the boundary) instead of NCG
+// LDS.32 that would hit only 8 distinct 16-byte bank groups per warp.
+template <int NCG>
+__device__ __forceinline__ void lds_words(const uint8_t* p, int mis, uint32_t (&x)[4]) {
+    const uint4* a = reinterpret_cast<const uint4*>(p - 4 * mis);
+    const uint4 c0 = a[0];
+    uint32_t t[8] = {c0.x, c0.y, c0.z, c0.w, 0u, 0u, 0u, 0u};
+    if (mis + NCG > 4) {
+        const uint4 c1 = a[1];
+        t[4] = c1.x;
+        t[5] = c1.y;
+        t[6] = c1.z;
+        t[7] = c1.w;
+    }
+#pragma unroll
+    for (int k = 0; k < NCG; ++k) x[k] = t[(mis + k) & 7];
+}
+
+// gather_chunk for records staged in shared memory (pack_one_tile): same
+// contract as gather_chunk with CHECK_ROWS = false, rows 0..31 of seq. PM =
+// (pitch / 4) % 4, so row i starts (i * PM) % 4 words past a 16-byte boundary
+// (group bases and col0 are 16-byte aligned). Per 8 rows and 4 columns: one
+// 8x8 byte-lane transpose (24 FMA + 24 LOP3) turns the 8 row words into the 8
+// bit planes of the ASCII bytes; bits 1/2/3 are the lo/hi/N planes and all
+// eight check the alphabet (7 LOP3, see the header).
+template <bool EDGE, int NCG, int PM, bool DEFER_N = false>
+__device__ __forceinline__ uint32_t gather_chunk_smem(const uint8_t* __restrict__ seq, size_t pitch,
+                                                      int col0, int m, uint32_t* __restrict__ dst,
+                                                      uint32_t* __restrict__ ndst, int dstride,
+                                                      uint32_t* __restrict__ nout = nullptr) {
+    uint32_t O[NCG][3][4];
+#pragma unroll
+    for (int cg = 0; cg < NCG; ++cg)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) O[cg][k][q] = 0u;
+    uint32_t err = 0u;
+    uint32_t cm[NCG];
+    if (EDGE) {
+#pragma unroll
+        for (int cg = 0; cg < NCG; ++cg) {
+            uint32_t mask = 0u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (col0 + 4 * cg + q < m) mask |= 0xFFu << (8 * q);
+            cm[cg] = mask;
+        }
+    }
+#pragma unroll 1
+    for (int g8 = 0; g8 < 4; ++g8) {
+        uint32_t v[8][4];
+        const uint8_t* base = seq + static_cast<size_t>(8 * g8) * pitch + col0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) lds_words<NCG>(base + i * pitch, (i * PM) & 3, v[i]);
+#pragma unroll
+        for (int cg = 0; cg < NCG; ++cg) {
+            uint32_t w[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                w[i] = EDGE ? lop3<0xE4>(v[i][cg], 0x41414141u, cm[cg]) : v[i][cg];
+            transpose8_bytes(w);
+            // bit i of byte q of w[k] = bit k of (row 8*g8+i, column 4cg+q)
+            const uint32_t e0 = lop3<0xFB>(w[5], w[6], w[7]);   // b5 | ~b6 | b7
+            const uint32_t t1 = lop3<0x51>(w[1], w[2], w[3]);   // ~b3 & (~b2 | b1)
+            const uint32_t t2 = lop3<0x04>(w[1], w[2], w[3]);   // b2 & ~b1 & ~b3
+            const uint32_t t3 = lop3<0x2A>(w[1], w[2], w[3]);   // b3 & ~(b2 & b1)
+            const uint32_t r1 = lop3<0xBE>(w[0], t1, e0);       // (b0 ^ t1) | e0
+            const uint32_t r2 = lop3<0xBE>(w[4], t2, r1);       // (b4 ^ t2) | r1
+            err = lop3<0xFE>(err, r2, t3);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    O[cg][k][q] = __byte_perm(O[cg][k][q], w[k + 1], 0x0321 | ((4 + q) << 12));
+        }
+    }
+#pragma unroll
+    for (int cg = 0; cg < NCG; ++cg)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int col = 4 * cg + q;
+            if constexpr (DEFER_N) nout[col] = O[cg][2][q];  // columns >= m read as 'A': 0
+            if (EDGE && col0 + col >= m) continue;  // never read: columns >= m are N
+            dst[(col * 2 + 0) * dstride] = O[cg][0][q];
+            dst[(col * 2 + 1) * dstride] = O[cg][1][q];
+            if constexpr (!DEFER_N) ndst[col * dstride] = O[cg][2][q];
+        }
+    return err;
+}
+
 // gather_chunk for nibble records (pack.cuh nibble format, validated on the
 // host): a 16-column chunk is two words per row; column group cg (4 columns)
 // is word cg/2, low nibbles for even cg, high nibbles for odd cg, so ASCII bit
