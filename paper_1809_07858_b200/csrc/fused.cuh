@@ -137,6 +137,10 @@ __device__ __forceinline__ void load_rel(const uint32_t* __restrict__ base,
     }
 }
 
+__device__ __forceinline__ void prefetch_l1(const uint32_t* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // One mismatch-map word D = !bases_match for a (pattern, text) column pair.
 // FAST: both N words are known zero (N-free warp, interior block): 2 LOP3.
 template <bool FAST>
@@ -341,6 +345,24 @@ __device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes
         const uint32_t* pbase = pb + static_cast<long long>(pcol0) * kLhColWords;
         const uint32_t* tnbase = tnb + static_cast<long long>(tcol0) * kNColWords;
         const uint32_t* pnbase = pnb + static_cast<long long>(pcol0) * kNColWords;
+        if (blk + 1 < NB) {
+            // pull the next block's first-touch columns (text tcol0+TW.., pattern
+            // pcol0+TW+2E.., 4 each) into L1 now: their loads then wait ~L1 latency
+            // instead of L2/DRAM latency (lo/hi words of a column are 64
+            // contiguous bytes of the pair block; these 4 columns span <= 3 lines)
+            const int nt = tcol0 + TW, np = pcol0 + TW + 2 * E;
+            const uint32_t* tn = tb + static_cast<long long>(max(nt, 0)) * kLhColWords;
+            const uint32_t* pn = pb + static_cast<long long>(max(np, 0)) * kLhColWords;
+            if (nt + B <= m) {
+                prefetch_l1(tn);
+                prefetch_l1(tn + 2 * kLhColWords);
+            }
+            if (np + B <= m) {
+                prefetch_l1(pn);
+                prefetch_l1(pn + 2 * kLhColWords);
+                prefetch_l1(pn + 3 * kLhColWords);
+            }
+        }
         if (interior)
             search_block<E, false, NCLOAD, NOPN>(tbase, tnbase, tcol0, pbase, pnbase, pcol0, m, Dc,
                                                  best);
