@@ -440,9 +440,10 @@ def run_ours(args, rank, world, local_rank):
         pack_traffic = None
         try:
             tj = json.load(open(tpath))
-            pack_traffic = float(tj["per_kernel_bytes"]["pack_tile_kernel<8,4,0>"]) * n / float(tj["pairs"])
+            pack_traffic = float(tj["per_kernel_bytes"]["pack_tile_kernel"]) * n / float(tj["pairs"])
+            search_traffic = float(tj["per_kernel_bytes"]["shouji_search_w4"]) * n / float(tj["pairs"])
         except Exception:
-            pack_traffic = None
+            pack_traffic = search_traffic = None
         # ASCII in; lo/hi planes x 2 sequences out, plus the N planes unless the pack
         # skips them (N-presence flags, pack.cuh: the synthetic config-1 data has no N)
         nflags = os.environ.get("PF_NFLAGS", "1") != "0"
@@ -454,14 +455,15 @@ def run_ours(args, rank, world, local_rank):
         windows = ((m + 3 + 3) // 4) * 4
         lop3_pair = ((2 * e + 1) * (6 if nflags else 7) + 2 * e * 10 + 19) * windows / 32
         roofline["per_kernel"] = [
-            {"kernel": "sb::pack_tile_kernel<8,4,0>", "ms": pk_ms, "share": pk_ms / (pk_ms + se_ms),
+            {"kernel": f"sb::pack_tile_kernel<8,{(pitch // 4) % 4},0,1>", "ms": pk_ms, "share": pk_ms / (pk_ms + se_ms),
              "bound": "hbm", "algorithmic_bytes_per_pair": pack_bytes / n,
              "achieved": pack_bytes / (pk_ms * 1e-3) / 1e9, "unit": "GB/s",
              "frac": pack_bytes / (pk_ms * 1e-3) / 1e9 / float(peaks["hbm_gbs"]),
              "traffic": pack_traffic},
             {"kernel": f"sb::shouji_search_w4<{e}>", "ms": se_ms, "share": se_ms / (pk_ms + se_ms),
              "bound": "int (ALU pipe, LOP3)", "algorithmic_lop3_per_pair": lop3_pair,
-             "achieved": lop3_pair * n / (se_ms * 1e-3), "unit": "lane-ops/s"},
+             "achieved": lop3_pair * n / (se_ms * 1e-3), "unit": "lane-ops/s",
+             "traffic": search_traffic},
         ]
     int_view = None
     if rank == 0:
