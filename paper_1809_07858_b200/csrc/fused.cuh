@@ -345,12 +345,16 @@ __device__ __forceinline__ void search_group(const uint32_t* __restrict__ planes
         const uint32_t* pbase = pb + static_cast<long long>(pcol0) * kLhColWords;
         const uint32_t* tnbase = tnb + static_cast<long long>(tcol0) * kNColWords;
         const uint32_t* pnbase = pnb + static_cast<long long>(pcol0) * kNColWords;
-        if (blk + 1 < NB) {
-            // pull the next block's first-touch columns (text tcol0+TW.., pattern
-            // pcol0+TW+2E.., 4 each) into L1 now: their loads then wait ~L1 latency
-            // instead of L2/DRAM latency (lo/hi words of a column are 64
-            // contiguous bytes of the pair block; these 4 columns span <= 3 lines)
-            const int nt = tcol0 + TW, np = pcol0 + TW + 2 * E;
+#ifndef SB_PF_DIST
+#define SB_PF_DIST 2
+#endif
+        if (blk + SB_PF_DIST < NB) {
+            // pull the first-touch columns of block blk + SB_PF_DIST (text
+            // tcol0+TW.., pattern pcol0+TW+2E.., 4 each, shifted by the distance)
+            // towards the SM now: their loads then wait on L2 instead of DRAM
+            // (lo/hi words of a column are 64 contiguous bytes of the pair block;
+            // these 4 columns span <= 3 lines)
+            const int nt = tcol0 + TW + B * (SB_PF_DIST - 1), np = pcol0 + TW + 2 * E + B * (SB_PF_DIST - 1);
             const uint32_t* tn = tb + static_cast<long long>(max(nt, 0)) * kLhColWords;
             const uint32_t* pn = pb + static_cast<long long>(max(np, 0)) * kLhColWords;
             if (nt + B <= m) {
