@@ -252,6 +252,44 @@ def test_device_configs(gpu, oracle, kind, m, es):
         assert (est.cpu().numpy().view(np.uint32) == e2).all()
 
 
+@pytest.mark.parametrize("m", [37, 100, 150, 250])
+def test_device_pitch_phases(gpu, oracle, m):
+    """Device records at every row phase (pitch mod 16 = 0, 4, 8, 12: the pack
+    kernel's compile-time row alignment, pack_tile.cuh) with garbage in the
+    padding bytes past m, which must be ignored; an illegal byte inside a record
+    is still found at every phase."""
+    import torch
+    rng = np.random.default_rng(m)
+    n = 3000
+    t, p = oracle.generate_pairs(m, n, m, 0, 10) if m == 100 else (None, None)
+    if t is None:
+        t = np.frombuffer(b"ACGTN", np.uint8)[rng.integers(0, 4, size=(n, m))].copy()
+        p = t.copy()
+        flip = rng.random((n, m)) < 0.05
+        p[flip] = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=int(flip.sum()))]
+    a0, e0, _ = oracle.shouji_batch(t, p, 5)
+    base = ((m + 3) // 4) * 4
+    for pitch in sorted({base, base + 4, base + 8, base + 12}):
+        ht = rng.integers(0, 256, size=(n, pitch), dtype=np.uint8)  # garbage padding
+        hp = rng.integers(0, 256, size=(n, pitch), dtype=np.uint8)
+        ht[:, :m] = t
+        hp[:, :m] = p
+        tt = torch.from_numpy(ht).cuda()
+        pt = torch.from_numpy(hp).cuda()
+        acc = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+        est = torch.zeros(n, dtype=torch.int32, device="cuda")
+        gpu.shouji_filter_device(tt.data_ptr(), pt.data_ptr(), pitch, n, m, 5, acc.data_ptr(),
+                                 d_estimates=est.data_ptr())
+        torch.cuda.synchronize()
+        assert (acc.cpu().numpy().view(np.uint32) == a0).all(), f"pitch {pitch}"
+        assert (est.cpu().numpy().view(np.uint32) == e0).all(), f"pitch {pitch}"
+        i, j = int(rng.integers(0, n)), int(rng.integers(0, m))
+        pt[i, j] = ord("x")
+        with pytest.raises(gpu.illegal_character_error) as ei:
+            gpu.shouji_filter_device(tt.data_ptr(), pt.data_ptr(), pitch, n, m, 5, acc.data_ptr())
+        assert (ei.value.pair, ei.value.field, ei.value.position()) == (i, 1, j)
+
+
 # --- errors --------------------------------------------------------------------------
 
 def test_illegal_characters(gpu):
