@@ -455,7 +455,7 @@ def run_ours(args, rank, world, local_rank):
         windows = ((m + 3 + 3) // 4) * 4
         lop3_pair = ((2 * e + 1) * (6 if nflags else 7) + 2 * e * 10 + 19) * windows / 32
         roofline["per_kernel"] = [
-            {"kernel": f"sb::pack_tile_kernel<8,{(pitch // 4) % 4},0,1>", "ms": pk_ms, "share": pk_ms / (pk_ms + se_ms),
+            {"kernel": f"sb::pack_tile_kernel<8,128,{(pitch // 4) % 4},0,1>", "ms": pk_ms, "share": pk_ms / (pk_ms + se_ms),
              "bound": "hbm", "algorithmic_bytes_per_pair": pack_bytes / n,
              "achieved": pack_bytes / (pk_ms * 1e-3) / 1e9, "unit": "GB/s",
              "frac": pack_bytes / (pk_ms * 1e-3) / 1e9 / float(peaks["hbm_gbs"]),

@@ -2,6 +2,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "pack.cuh"
@@ -11,11 +13,11 @@ namespace sb {
 
 namespace {
 
-// One CTA per tile of GROUPS x 32 pairs (pack_one_tile, pack_tile.cuh).
-// NFLAG: also write the N-presence flags (pack.cuh) and skip N-free tiles' N planes.
-// 4 CTAs/SM (128 registers): ptxas would otherwise take up to 180 and fit 2.
-template <int GROUPS, int PM, bool NIB, bool NFLAG = false>
-__global__ void __launch_bounds__(kPackNT, 4)
+// One CTA of NT threads per tile of GROUPS x 32 pairs (pack_one_tile,
+// pack_tile.cuh). NFLAG: also write the N-presence flags (pack.cuh) and skip
+// N-free tiles' N planes. 128 registers: ptxas would otherwise take up to 180.
+template <int GROUPS, int NT, int PM, bool NIB, bool NFLAG = false>
+__global__ void __launch_bounds__(NT, 512 / NT)
 pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
                  size_t pitch, long long n, int m, uint32_t* __restrict__ planes,
                  uint32_t* __restrict__ err_flag, uint32_t* __restrict__ nflags) {
@@ -25,10 +27,10 @@ pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ p
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     if (NFLAG && blockIdx.x == 0) {  // the all-zero N column image N-free groups read
         uint32_t* zero = nflags + nflag_words(n);
-        for (int i = threadIdx.x; i < static_cast<int>(nzero_words(m)); i += kPackNT) zero[i] = 0u;
+        for (int i = threadIdx.x; i < static_cast<int>(nzero_words(m)); i += NT) zero[i] = 0u;
     }
     __syncthreads();
-    const uint32_t err = pack_one_tile<PM, kPackNT, NIB, NFLAG>(
+    const uint32_t err = pack_one_tile<PM, NT, NIB, NFLAG>(
         sm, &bar, 0, GROUPS, static_cast<long long>(blockIdx.x) * GROUPS, text, pattern, pitch, n, m,
         planes, nflags, sflag);
     if (!NIB && err) atomicOr(err_flag, 1u);
@@ -61,34 +63,75 @@ pack_direct_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__
 
 }  // namespace
 
-template <int GROUPS, int PM, bool NIB = false, bool NFLAG = false>
+// Tile geometry: `groups` record groups per CTA of `nt` threads, one
+// (chunk, group, sequence) item per thread (2 * groups * ceil(m/16) <= nt),
+// chosen so most threads hold an item and 3-4 CTAs' tiles fit one SM's shared
+// memory (measured, tools/exp_stages.py with PF_PACK_GEOM): C = ceil(m/16) <= 8
+// (m <= 128) 8 groups x 128 threads; C <= 12 4 x 96 (m=150: 1.16 ms per 16M
+// pairs vs 1.33 for 4 x 128, 1.24 for 6 x 128, 1.29 for 8 x 160); otherwise
+// 4 x 128 (m=250: 1.02 ms per 8M pairs vs 1.33 for 3 x 96 or 2 x 64).
+// PF_PACK_GEOM="groups,threads" picks another compiled geometry (A/B runs).
+struct TileGeom {
+    int groups, nt;
+};
+static TileGeom tile_geom(size_t pitch, int m) {
+    if (const char* e = std::getenv("PF_PACK_GEOM")) {
+        int g = 0, t = 0;
+        if (std::sscanf(e, "%d,%d", &g, &t) == 2 &&
+            ((g == 8 && t == 128) || (g == 4 && t == 96) || (g == 4 && t == 128)))
+            return {g, t};
+    }
+    const int C = (m + CH - 1) / CH;
+    if (C <= 8 && tile_smem(pitch, 8) <= 110 * 1024) return {8, 128};
+    if (C <= 12) return {4, 96};
+    return {4, 128};
+}
+
+template <int GROUPS, int NT, int PM, bool NIB = false, bool NFLAG = false>
 static cudaError_t launch_tile_f(const uint8_t* text, const uint8_t* pattern, size_t pitch,
                                  long long n, int m, uint32_t* planes, uint32_t* err_flag,
                                  uint32_t* nflags, cudaStream_t s) {
-    const cudaError_t st = ensure_smem_attr<pack_tile_kernel<GROUPS, PM, NIB, NFLAG>>(110 * 1024);
+    const cudaError_t st =
+        ensure_smem_attr<pack_tile_kernel<GROUPS, NT, PM, NIB, NFLAG>>(110 * 1024);
     if (st != cudaSuccess) return st;
     const long long ngroups = (n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + GROUPS - 1) / GROUPS);
-    pack_tile_kernel<GROUPS, PM, NIB, NFLAG><<<grid, kPackNT, tile_smem(pitch, GROUPS), s>>>(
+    pack_tile_kernel<GROUPS, NT, PM, NIB, NFLAG><<<grid, NT, tile_smem(pitch, GROUPS), s>>>(
         text, pattern, pitch, n, m, planes, err_flag, nflags);
     return cudaGetLastError();
 }
 
-template <int GROUPS, int PM, bool NIB = false>
+template <int PM, bool NIB = false, bool NFLAG = false>
+static cudaError_t launch_tile_nt(const uint8_t* text, const uint8_t* pattern, size_t pitch,
+                                  long long n, int m, TileGeom tg, uint32_t* planes,
+                                  uint32_t* err_flag, uint32_t* nflags, cudaStream_t s) {
+    if (tg.groups == 8)
+        return launch_tile_f<8, 128, PM, NIB, NFLAG>(text, pattern, pitch, n, m, planes, err_flag, nflags, s);
+    if (tg.nt == 96)
+        return launch_tile_f<4, 96, PM, NIB, NFLAG>(text, pattern, pitch, n, m, planes, err_flag, nflags, s);
+    return launch_tile_f<4, 128, PM, NIB, NFLAG>(text, pattern, pitch, n, m, planes, err_flag, nflags, s);
+}
+
+template <int PM, bool NIB = false>
 static cudaError_t launch_tile(const uint8_t* text, const uint8_t* pattern, size_t pitch,
                                long long n, int m, uint32_t* planes, uint32_t* err_flag,
                                uint32_t* nflags, cudaStream_t s) {
-    return nflags ? launch_tile_f<GROUPS, PM, NIB, true>(text, pattern, pitch, n, m, planes,
-                                                            err_flag, nflags, s)
-                  : launch_tile_f<GROUPS, PM, NIB, false>(text, pattern, pitch, n, m, planes,
-                                                             err_flag, nullptr, s);
+    const TileGeom tg = tile_geom(pitch, m);
+    return nflags ? launch_tile_nt<PM, NIB, true>(text, pattern, pitch, n, m, tg, planes,
+                                                  err_flag, nflags, s)
+                  : launch_tile_nt<PM, NIB, false>(text, pattern, pitch, n, m, tg, planes,
+                                                   err_flag, nullptr, s);
 }
 
 // The tile kernels can write N-presence flags when each thread owns at most
 // one (chunk, group, sequence) item.
+static bool tile_fits(size_t pitch, int m) {
+    const TileGeom tg = tile_geom(pitch, m);
+    return tile_smem(pitch, tg.groups) <= 110 * 1024;
+}
 static bool tile_nflags_fit(size_t pitch, int m) {
-    const int groups = tile_groups(pitch);
-    return tile_smem(pitch, groups) <= 110 * 1024 && 2 * groups * ((m + CH - 1) / CH) <= kPackNT;
+    const TileGeom tg = tile_geom(pitch, m);
+    return tile_fits(pitch, m) && 2 * tg.groups * ((m + CH - 1) / CH) <= tg.nt;
 }
 
 bool pack_writes_nflags(const FilterArgs& a) {
@@ -104,26 +147,14 @@ cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitc
     if (n <= 0) return cudaSuccess;
     if (pitch % 4 != 0) return cudaErrorInvalidValue;
     if (nflags && (!planes || !tile_nflags_fit(pitch, m))) return cudaErrorInvalidValue;
-    const int groups = tile_groups(pitch);
-    const size_t smem = tile_smem(pitch, groups);
     cudaError_t st;
-    if (smem <= 110 * 1024) {
+    if (tile_fits(pitch, m)) {
         // row i of a group starts (i * pm) % 4 words past a 16-byte boundary
-        const int pm = static_cast<int>((pitch / 4) % 4);
-        if (groups == 8) {
-            switch (pm) {
-                case 0: st = launch_tile<8, 0>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
-                case 1: st = launch_tile<8, 1>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
-                case 2: st = launch_tile<8, 2>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
-                default: st = launch_tile<8, 3>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
-            }
-        } else {
-            switch (pm) {
-                case 0: st = launch_tile<4, 0>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
-                case 1: st = launch_tile<4, 1>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
-                case 2: st = launch_tile<4, 2>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
-                default: st = launch_tile<4, 3>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
-            }
+        switch ((pitch / 4) % 4) {
+            case 0: st = launch_tile<0>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+            case 1: st = launch_tile<1>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+            case 2: st = launch_tile<2>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
+            default: st = launch_tile<3>(text, pattern, pitch, n, m, planes, err_flag, nflags, s); break;
         }
     } else {
         const long long items = 2 * ((n + 31) / 32) * ((plane_cols(m) + CH - 1) / CH);
@@ -137,7 +168,7 @@ cudaError_t launch_pack(const uint8_t* text, const uint8_t* pattern, size_t pitc
 
 bool nibble_pack_fits(int m) {
     const size_t np = nibble_pitch(m);
-    return tile_smem(np, tile_groups(np)) <= 110 * 1024;
+    return tile_fits(np, m);
 }
 
 cudaError_t launch_pack_nibbles(const uint8_t* text, const uint8_t* pattern, long long n, int m,
@@ -146,10 +177,7 @@ cudaError_t launch_pack_nibbles(const uint8_t* text, const uint8_t* pattern, lon
     if (!nibble_pack_fits(m) || planes == nullptr) return cudaErrorInvalidValue;
     const size_t np = nibble_pitch(m);
     if (nflags && !tile_nflags_fit(np, m)) return cudaErrorInvalidValue;
-    const cudaError_t st =
-        tile_groups(np) == 8
-            ? launch_tile<8, 0, true>(text, pattern, np, n, m, planes, nullptr, nflags, s)
-            : launch_tile<4, 0, true>(text, pattern, np, n, m, planes, nullptr, nflags, s);
+    const cudaError_t st = launch_tile<0, true>(text, pattern, np, n, m, planes, nullptr, nflags, s);
     count_launch();
     return st;
 }

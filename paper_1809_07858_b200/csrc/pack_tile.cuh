@@ -57,7 +57,6 @@ __host__ __device__ inline size_t seq_stride(size_t pitch, int groups) {
     return groups * group_stride(pitch) + 64;
 }
 inline size_t tile_smem(size_t pitch, int groups) { return 2 * seq_stride(pitch, groups) + 128; }
-inline int tile_groups(size_t pitch) { return pitch <= 128 ? 8 : 4; }
 
 template <bool EDGE, int PM, bool NIB = false, bool DEFER_N = false>
 __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size_t pitch, int col0,
