@@ -49,12 +49,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // Shared-memory image of one tile: for each (sequence, group) the group's 32
 // records, contiguous (one bulk copy each). Consecutive groups are offset by
-// an extra 16 bytes and the pattern half by 64, so the 8 lanes of a
-// quarter-warp (2 sequences x 4 groups reading the same row/column offset) hit
-// 8 distinct 16-byte bank groups in their LDS.128.
+// an extra 16 bytes (32 * pitch is a multiple of 128) and the pattern half
+// starts 64 bytes past a 128-byte multiple of the text half, so the 8 lanes
+// of a quarter-warp (2 sequences x 4 groups reading the same row/column
+// offset) hit 8 distinct 16-byte bank groups in their LDS.128.
 __host__ __device__ inline size_t group_stride(size_t pitch) { return 32 * pitch + 16; }
 __host__ __device__ inline size_t seq_stride(size_t pitch, int groups) {
-    return groups * group_stride(pitch) + 64;
+    return groups * group_stride(pitch) + 16 * ((4 - groups) & 7);
 }
 inline size_t tile_smem(size_t pitch, int groups) { return 2 * seq_stride(pitch, groups) + 128; }
 
