@@ -129,6 +129,15 @@ class Oracle:
             raise OracleError(st)
         return t, p
 
+    def substitution_pairs(self, seed, count, m, max_subs):
+        """Restated substitution_pairs (acceptance_tests.cpp:252-276, criterion 7)
+        -> (text u8[count, m], pattern u8[count, m])."""
+        t = np.zeros((count, m), np.uint8)
+        p = np.zeros((count, m), np.uint8)
+        self.lib.so_substitution_pairs(C.c_uint64(seed), C.c_size_t(count), C.c_size_t(m),
+                                       C.c_uint32(max_subs), _ptr(t), _ptr(p), C.c_size_t(m))
+        return t, p
+
     def banded_edit_distance(self, pattern: bytes, text: bytes, e: int) -> int:
         return self.lib.so_banded_edit_distance(pattern, text, len(text), e)
 

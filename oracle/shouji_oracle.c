@@ -370,6 +370,32 @@ int so_generate_pairs(uint64_t seed, size_t count, size_t len, uint32_t lo, uint
     return SO_OK;
 }
 
+/* substitution_pairs — proj/tests/acceptance_tests.cpp:252-276 (criterion 7's
+ * substitution-only sets): per pair, text = m uniform bases (rng()%4); k =
+ * rng() % (max_subs+1); k times: pos = rng()%m, then draw bases (rng()%4)
+ * until one differs from pattern[pos] and write it. Same mt19937_64 stream
+ * as generate_pairs. */
+void so_substitution_pairs(uint64_t seed, size_t count, size_t m, uint32_t max_subs, char* text,
+                           char* pattern, size_t stride) {
+    static const char bases[4] = {'A', 'C', 'G', 'T'};
+    so_mt64* rng = (so_mt64*)malloc(sizeof(so_mt64));
+    mt64_seed(rng, seed);
+    for (size_t p = 0; p < count; ++p) {
+        char* t = text + p * stride;
+        char* q = pattern + p * stride;
+        for (size_t i = 0; i < m; ++i) t[i] = bases[mt64_next(rng) % 4];
+        memcpy(q, t, m);
+        const uint32_t k = (uint32_t)(mt64_next(rng) % ((uint64_t)max_subs + 1));
+        for (uint32_t j = 0; j < k; ++j) {
+            const size_t pos = (size_t)(mt64_next(rng) % m);
+            char ch = bases[mt64_next(rng) % 4];
+            while (ch == q[pos]) ch = bases[mt64_next(rng) % 4];
+            q[pos] = ch;
+        }
+    }
+    free(rng);
+}
+
 /* banded_edit_distance — proj/src/edit_distance.cpp:26-70, restated as the
  * plain full DP clipped at e+1 (equal lengths; N never matches). Returns the
  * distance, or -1 when it exceeds e. Used only for eval-style tests. */

@@ -138,6 +138,48 @@ def test_acceptance_criterion2(gpu, oracle, m, e, lost):
     assert int((z["similar"] & ~bitmap_bools(acc, 100_000)).sum()) == lost
 
 
+def test_acceptance_criterion3_exact_at_zero(gpu, oracle):
+    # acceptance_tests.cpp:132-146: at e=0 the GPU decision is equality (3407/10000 identical)
+    t, p = oracle.generate_pairs(3300, 10_000, 100, 0, 2)
+    same = (t == p).all(axis=1)
+    acc, _, _ = gpu.shouji_filter_batch(t, p, 0)
+    assert int(same.sum()) == 3407 and (bitmap_bools(acc, 10_000) == same).all()
+
+
+def test_acceptance_criterion5_width_trend(gpu, oracle):
+    # acceptance_tests.cpp:180-203 on the GPU: width 4 loses 631 similar pairs of
+    # criterion 2's sets, widths 5+6 lose 30,783 (proj/test_output.txt:19)
+    lost4 = lost56 = 0
+    for m, e in [(100, 2), (100, 5), (150, 7), (250, 15)]:
+        z = np.load(os.path.join(GOLD, f"fr_m{m}_e{e}.npz"))
+        t, p = oracle.generate_pairs(int(z["seed"]), 100_000, m, 0, e)
+        for w in (4, 5, 6):
+            acc, est, _ = gpu.shouji_filter_batch(t, p, e, w, estimates=True)
+            if w != 4:  # bit-exact with the oracle at the wider widths as well
+                a2, e2, _ = oracle.shouji_batch(t, p, e, w)
+                assert (acc == a2).all() and (est == e2).all(), (m, e, w)
+            lost = int((z["similar"] & ~bitmap_bools(acc, 100_000)).sum())
+            if w == 4:
+                lost4 += lost
+            else:
+                lost56 += lost
+    assert (lost4, lost56) == (631, 30_783)
+
+
+@pytest.mark.parametrize("seed,e,subs_hi,fa_rate", [(7702, 2, 4, 0.257745), (7705, 5, 10, 0.643066)])
+def test_acceptance_criterion7_rate_structure(gpu, oracle, seed, e, subs_hi, fa_rate):
+    # acceptance_tests.cpp:246-310 evaluated entirely on the GPU: Shouji decisions and
+    # the banded edit-distance oracle (evaluate.cpp:50-79); MAGNET bit-exact with the oracle
+    t, p = oracle.substitution_pairs(seed, 20_000, 100, subs_hi)
+    a = bitmap_bools(gpu.shouji_filter_batch(t, p, e)[0], 20_000)
+    within = gpu.banded_edit_distance_batch(t, p, e) >= 0
+    assert round(float((a & ~within).sum()) / float((~within).sum()), 6) == fa_rate
+    assert int((~a & within).sum()) == 0
+    ma, me, _ = gpu.magnet_filter_batch(t, p, e, estimates=True)
+    oa, oe, _ = oracle.magnet_batch(t, p, e)
+    assert (ma == oa).all() and (me == oe).all()
+
+
 # --- sweeps over E, widths, lengths -------------------------------------------------
 
 @pytest.mark.parametrize("e", list(range(0, 32)))

@@ -166,6 +166,50 @@ def test_acceptance_criterion2_counts(oracle, m, e, lost):
     assert int((z["similar"] & ~a).sum()) == lost
 
 
+def _bools(acc, n):
+    return np.unpackbits(np.ascontiguousarray(acc).view(np.uint8), bitorder="little")[:n].astype(bool)
+
+
+def test_acceptance_criterion3_exact_at_zero(oracle):
+    # acceptance_tests.cpp:132-146 (criterion 3): at e=0 the decision is equality;
+    # SURVEY 8(c) records 3407/10000 identical pairs, 0 violations
+    t, p = oracle.generate_pairs(3300, 10_000, 100, 0, 2)
+    same = (t == p).all(axis=1)
+    acc, _, _ = oracle.shouji_batch(t, p, 0)
+    assert int(same.sum()) == 3407
+    assert (_bools(acc, 10_000) == same).all()
+
+
+def test_acceptance_criterion5_width_trend(oracle):
+    # acceptance_tests.cpp:180-203 (criterion 5): over criterion 2's similar pairs,
+    # width 4 loses 631 (= 583+41+7+0) and widths 5+6 lose 30,783 (proj/test_output.txt:19)
+    lost4 = lost56 = 0
+    for m, e in [(100, 2), (100, 5), (150, 7), (250, 15)]:
+        z = np.load(os.path.join(GOLD, f"fr_m{m}_e{e}.npz"))
+        t, p = oracle.generate_pairs(int(z["seed"]), 100_000, m, 0, e)
+        for w in (4, 5, 6):
+            acc, _, _ = oracle.shouji_batch(t, p, e, w, estimates=False)
+            lost = int((z["similar"] & ~_bools(acc, 100_000)).sum())
+            if w == 4:
+                lost4 += lost
+            else:
+                lost56 += lost
+    assert (lost4, lost56) == (631, 30_783)
+
+
+@pytest.mark.parametrize("seed,e,subs_hi,fa_rate", [(7702, 2, 4, 0.257745), (7705, 5, 10, 0.643066)])
+def test_acceptance_criterion7_rate_structure(oracle, seed, e, subs_hi, fa_rate):
+    # acceptance_tests.cpp:246-310 (criterion 7): substitution-only pairs, evaluate()
+    # (evaluate.cpp:50-79): fa_rate = false accepts / oracle rejects, printed with
+    # std::to_string (6 decimals); Shouji never rejects a similar pair here
+    t, p = oracle.substitution_pairs(seed, 20_000, 100, subs_hi)
+    a = _bools(oracle.shouji_batch(t, p, e, estimates=False)[0], 20_000)
+    within = np.array([oracle.banded_edit_distance(p[i].tobytes(), t[i].tobytes(), e) >= 0
+                       for i in range(20_000)])
+    assert round(float((a & ~within).sum()) / float((~within).sum()), 6) == fa_rate
+    assert int((~a & within).sum()) == 0
+
+
 # --- the reference library itself (build container only) -------------------------
 
 def test_oracle_vs_reference_random(oracle, reference):
