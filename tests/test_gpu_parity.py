@@ -363,6 +363,29 @@ def test_illegal_characters(gpu):
             gpu.shouji_filter_batch(q, t[:64], 5)
 
 
+@pytest.mark.parametrize("m", [37, 100, 150])
+def test_every_byte_value_device_pack(gpu, m):
+    """The device pack kernel's alphabet check (8x8 transposes + 7 LOP3, phase_a.cuh)
+    over all 256 byte values, at positions spread over every 16-column chunk (the
+    straddling one included), in text and pattern: an error exactly for bytes
+    outside A/C/G/T/N (lowercase too, packed_sequence.cpp:19-29), reported at the
+    right (pair, field, position)."""
+    rng = np.random.default_rng(m)
+    n = 64
+    t = np.frombuffer(b"ACGTN", np.uint8)[rng.integers(0, 5, size=(n, m))].copy()
+    p = np.frombuffer(b"ACGTN", np.uint8)[rng.integers(0, 5, size=(n, m))].copy()
+    for b in range(256):
+        pair, field, pos = b % n, b % 2, (b * 7) % m
+        tt, pp = t.copy(), p.copy()
+        (tt if field == 0 else pp)[pair, pos] = b
+        if bytes([b]) in (b"A", b"C", b"G", b"T", b"N"):
+            gpu.shouji_filter_batch(tt, pp, 3)
+            continue
+        with pytest.raises(gpu.illegal_character_error) as ei:
+            gpu.shouji_filter_batch(tt, pp, 3)
+        assert (ei.value.pair, ei.value.field, ei.value.position()) == (pair, field, pos), b
+
+
 def test_empty_sequence(gpu):
     with pytest.raises(gpu.empty_sequence_error):
         gpu.shouji_filter_batch(np.zeros((4, 0), np.uint8), np.zeros((4, 0), np.uint8), 1, m=0)
