@@ -16,9 +16,11 @@
 // (bitvector.hpp:88-91) — with no special cases in phase B.
 //
 // Validation is exact and costs no extra pass: a byte is in {A,C,G,T,N} iff
-// bits 7..5 are 010 (raw OR/AND accumulators over the loaded words) and,
-// given (b3,b2,b1) in {000,001,011,010,111}, b0 == ~b3&(~b2|b1) and
-// b4 == b2&~b1&~b3 (checked on the gathered planes). Any failure only raises a
+// bits 7..5 are 010 and, given (b3,b2,b1) in {000,001,011,010,111},
+// b0 == ~b3&(~b2|b1) and b4 == b2&~b1&~b3. gather_chunk_smem (the shared-memory
+// tile path) checks all eight bits on its transposed bit planes; gather_chunk
+// (global-memory path) checks bits 7..5 with OR/AND accumulators over the
+// loaded words and bits 0..4 on its gathered planes. Any failure only raises a
 // flag; the host then runs a locator kernel for the reference's exact error
 // (lowest pair, text before pattern, lowest position).
 #pragma once
