@@ -212,6 +212,21 @@ def test_acceptance_criterion7_rate_structure(oracle, seed, e, subs_hi, fa_rate)
 
 # --- the reference library itself (build container only) -------------------------
 
+def test_reference_unit_tests_pass_on_ref_build():
+    # The reference's own unit tests (proj/tests/test_*.cpp except test_cli.cpp),
+    # compiled unmodified against our doctest-compatible shim and linked with the
+    # same objects as oracle/_ref: 80 cases, 175,923 checks, 0 failures
+    import subprocess
+    if not os.path.exists("/root/reference/proj/tests/test_shouji.cpp"):
+        pytest.skip("reference tests absent (GPU box)")
+    odir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle")
+    subprocess.run(["make", "-s", "-C", odir, "unit"], check=True, capture_output=True)
+    r = subprocess.run([os.path.join(odir, "_ref", "unit_tests")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.split() == ["cases", "80", "checks", "175923", "failures", "0",
+                                "failed_cases", "0"], r.stdout
+
+
 def test_oracle_vs_reference_random(oracle, reference):
     rng = np.random.default_rng(7)
     for m, e, w in [(100, 5, 4), (150, 7, 4), (250, 25, 4), (64, 31, 4), (100, 5, 6), (33, 3, 3)]:
