@@ -61,6 +61,12 @@ struct DeviceState {
     uint8_t* d_nib[2] = {nullptr, nullptr};
     size_t d_nib_bytes[2] = {0, 0};
     cudaEvent_t nib_ev[2] = {nullptr, nullptr};
+    // host-pack path: a copy stream for the chunk uploads, so chunk i+1's DMA
+    // overlaps chunk i's kernels; kern_ev[b]: the kernels that read device
+    // buffer b are done (before the next upload into it); up_ev: ordering point
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t kern_ev[2] = {nullptr, nullptr};
+    cudaEvent_t up_ev = nullptr;
     uint8_t* h_nrow[2] = {nullptr, nullptr};  // dibit path: pinned N-plane rows
     size_t h_nrow_bytes = 0;
     uint8_t* d_nrow[2] = {nullptr, nullptr};
@@ -331,7 +337,20 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             if (!d.nib_ev[b] &&
                 !cu(cudaEventCreateWithFlags(&d.nib_ev[b], cudaEventDisableTiming), "event"))
                 return;
+            if (!d.kern_ev[b] &&
+                !cu(cudaEventCreateWithFlags(&d.kern_ev[b], cudaEventDisableTiming), "event"))
+                return;
         }
+        if (!d.copy_stream &&
+            !cu(cudaStreamCreateWithFlags(&d.copy_stream, cudaStreamNonBlocking), "copy stream"))
+            return;
+        if (!d.up_ev && !cu(cudaEventCreateWithFlags(&d.up_ev, cudaEventDisableTiming), "event"))
+            return;
+        // uploads start after everything already queued on the device stream
+        // (earlier batches' kernels may still read the device record buffers)
+        if (!cu(cudaEventRecord(d.up_ev, d.stream), "record event") ||
+            !cu(cudaStreamWaitEvent(d.copy_stream, d.up_ev, 0), "copy stream order"))
+            return;
         if (!magnet &&
             !cu(grow(d.d_scratch, d.scratch_words, sb::planes_scratch_words(chunk, m)),
                 "alloc planes"))
@@ -365,20 +384,27 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
                 return fail(PF_ERR_ILLEGAL_CHARACTER);
             }
             const size_t cb = static_cast<size_t>(cn) * rp;
-            if (!cu(xfer(d.d_nib[b], ht, cb, cudaMemcpyHostToDevice, d.stream), "H2D records"))
+            // device buffer b is free once chunk i-2's kernels (which read it) are done
+            if (i >= 2 && !cu(cudaStreamWaitEvent(d.copy_stream, d.kern_ev[b], 0), "buffer order"))
+                return;
+            if (!cu(xfer(d.d_nib[b], ht, cb, cudaMemcpyHostToDevice, d.copy_stream), "H2D records"))
                 return;
             if (!cu(xfer(d.d_nib[b] + static_cast<size_t>(chunk) * rp, hq, cb,
-                         cudaMemcpyHostToDevice, d.stream), "H2D records"))
+                         cudaMemcpyHostToDevice, d.copy_stream), "H2D records"))
                 return;
             if (has_n) {
                 const size_t nb = static_cast<size_t>(cn) * npr;
-                if (!cu(xfer(d.d_nrow[b], hnt, nb, cudaMemcpyHostToDevice, d.stream), "H2D N rows"))
+                if (!cu(xfer(d.d_nrow[b], hnt, nb, cudaMemcpyHostToDevice, d.copy_stream),
+                        "H2D N rows"))
                     return;
                 if (!cu(xfer(d.d_nrow[b] + static_cast<size_t>(chunk) * npr, hnq, nb,
-                             cudaMemcpyHostToDevice, d.stream), "H2D N rows"))
+                             cudaMemcpyHostToDevice, d.copy_stream), "H2D N rows"))
                     return;
             }
-            if (!cu(cudaEventRecord(d.nib_ev[b], d.stream), "record event")) return;
+            // nib_ev[b]: this upload is done (host buffer b reusable; kernels may read)
+            if (!cu(cudaEventRecord(d.nib_ev[b], d.copy_stream), "record event") ||
+                !cu(cudaStreamWaitEvent(d.stream, d.nib_ev[b], 0), "upload order"))
+                return;
             if (magnet) {
                 if (!cu(sb::launch_magnet_dibits(
                             d.d_nib[b], d.d_nib[b] + static_cast<size_t>(chunk) * rp,
@@ -389,6 +415,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
                             bits ? d.d_bits + static_cast<size_t>(lo) * wpp : nullptr, d.stream),
                         "magnet kernel"))
                     return;
+                if (!cu(cudaEventRecord(d.kern_ev[b], d.stream), "record event")) return;
                 continue;
             }
             sb::FilterArgs a{};
@@ -408,6 +435,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             a.planes = d.d_scratch;
             a.planes_words = d.scratch_words;
             if (!cu(sb::launch_filter(a, d.stream), "filter kernel")) return;
+            if (!cu(cudaEventRecord(d.kern_ev[b], d.stream), "record event")) return;
         }
         if (!cu(scratch_release(d, d.stream), "scratch order")) return;
         if (!cu(xfer(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
@@ -849,6 +877,12 @@ void pf_ctx_destroy(pf_ctx* ctx) {
             if (d.h_pk[b]) cudaFreeHost(d.h_pk[b]);
             cudaFree(d.d_pk[b]);
             if (d.pk_ev[b]) cudaEventDestroy(d.pk_ev[b]);
+            if (d.kern_ev[b]) cudaEventDestroy(d.kern_ev[b]);
+        }
+        if (d.up_ev) cudaEventDestroy(d.up_ev);
+        if (d.copy_stream) {
+            cudaStreamSynchronize(d.copy_stream);
+            cudaStreamDestroy(d.copy_stream);
         }
         for (int b = 0; b < 2; ++b) {
             if (d.h_stage[b]) cudaFreeHost(d.h_stage[b]);
