@@ -259,7 +259,9 @@ int pf_generate_device(pf_ctx* ctx, int kind, uint64_t seed, uint32_t param, uin
 typedef struct pf_dataset pf_dataset;
 
 /* load_pairs (proj/src/dataset.cpp:13-44): one TEXT '\t' PATTERN pair per
- * line. Byte validation runs on the ctx's GPU; errors are the ones the
+ * line. The scan and the byte validation run on the host cores (ctx is not
+ * used and may be NULL; the records are then filtered on a ctx's GPUs by the
+ * batch calls); errors are the ones the
  * reference's line-by-line loader throws first: PF_ERR_PARSE with err->line for
  * a wrong field count, an empty field or an illegal byte (err->position/byte),
  * PF_ERR_LENGTH_MISMATCH with err->line for unequal lengths, PF_ERR_PARSE line

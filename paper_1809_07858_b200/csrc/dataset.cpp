@@ -4,19 +4,22 @@
 // Reference: load_pairs / load_pairs_file / write_pairs / generate_pairs,
 // proj/src/dataset.cpp:13-126 (declared proj/include/prefilter/dataset.hpp).
 //
-// Records are kept as fixed-stride ASCII (stride = m) in pinned host memory, so
-// a dataset can be handed to pf_shouji_filter_batch without another copy.
-// Character validation is NOT done on the host: the records are sent through
-// the GPU validation kernels (the same exact check the filter runs) and the
-// device's first illegal byte (lowest pair, text before pattern, lowest
-// position) is mapped back to its line. Structural checks (tabs, empty fields,
-// lengths) are a host scan. The error reported is the one the reference's
-// line-by-line loader would throw first:
+// Records are kept as fixed-stride ASCII (stride = m) in pageable host memory
+// (huge pages), so a dataset can be handed to pf_shouji_filter_batch without
+// another copy. The line scan (two parallel passes: count, then fill) and the
+// structural checks (tabs, empty fields, lengths) run on the host cores; the
+// well-formed prefix's bytes are checked with the host pack's exact AVX-512
+// alphabet test on the same worker pool, and the first illegal byte (lowest
+// pair, text before pattern, lowest position) is mapped back to its line. The
+// error reported is the one the reference's line-by-line loader would throw
+// first:
 //   per line: field count -> text codec (empty, then bytes) -> pattern codec
 //   -> text/pattern length -> dataset length; then "no pairs in input".
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -26,7 +29,13 @@
 #include <thread>
 #include <vector>
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include "../../include/shouji_b200.h"
+#include "host_pack.h"
 
 struct pf_dataset {
     uint8_t* text = nullptr;  // n x m, pinned when possible
@@ -39,6 +48,22 @@ struct pf_dataset {
 
 namespace {
 
+// PF_TRACE=1: phase timings of the loader on stderr (diagnostics)
+struct Trace {
+    bool on = [] {
+        const char* e = std::getenv("PF_TRACE");
+        return e && e[0] == '1';
+    }();
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[pf_dataset] %-22s %8.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 void set_parse(pf_error* err, int status, uint64_t line, const std::string& msg) {
     if (!err) return;
     err->status = status;
@@ -46,25 +71,22 @@ void set_parse(pf_error* err, int status, uint64_t line, const std::string& msg)
     std::snprintf(err->message, sizeof(err->message), "%s", msg.c_str());
 }
 
+// Records live in pageable memory (2 MiB-aligned, transparent huge pages):
+// pinning a multi-GB dataset costs ~0.45 s/GB, and the batch entry points
+// read pageable records as fast (host-pack path) or stage them.
 bool alloc_records(pf_dataset* ds, size_t n, uint32_t m) {
-    const size_t bytes = std::max<size_t>(n * m, 1);
-    void* t = nullptr;
-    void* p = nullptr;
-    if (cudaHostAlloc(&t, bytes, cudaHostAllocPortable) == cudaSuccess &&
-        cudaHostAlloc(&p, bytes, cudaHostAllocPortable) == cudaSuccess) {
-        ds->pinned = true;
-    } else {
-        cudaGetLastError();
-        if (t) cudaFreeHost(t);
-        t = std::malloc(bytes);
-        p = std::malloc(bytes);
-        ds->pinned = false;
-        if (!t || !p) {
-            std::free(t);
-            std::free(p);
-            return false;
-        }
+    const size_t al = size_t(1) << 21;
+    const size_t bytes = (std::max<size_t>(n * m, 1) + al - 1) / al * al;
+    void* t = std::aligned_alloc(al, bytes);
+    void* p = std::aligned_alloc(al, bytes);
+    if (!t || !p) {
+        std::free(t);
+        std::free(p);
+        return false;
     }
+    madvise(t, bytes, MADV_HUGEPAGE);
+    madvise(p, bytes, MADV_HUGEPAGE);
+    ds->pinned = false;
     ds->text = static_cast<uint8_t*>(t);
     ds->pattern = static_cast<uint8_t*>(p);
     ds->n = n;
@@ -100,10 +122,17 @@ struct line_info {
     int tabs = 0;                        // 1 = well-formed field count
 };
 
-// Split [begin, end) of buf into lines (std::getline semantics: a final
-// unterminated line counts, a trailing '\n' does not start a new line).
-void scan_lines(const char* buf, size_t begin, size_t end, std::vector<line_info>& out) {
-    size_t pos = begin;
+// Lines of [begin, end) of buf (std::getline semantics: a final unterminated
+// line counts, a trailing '\n' does not start a new line).
+size_t count_lines(const char* buf, size_t begin, size_t end) {
+    if (begin >= end) return 0;
+    const size_t nl = static_cast<size_t>(std::count(buf + begin, buf + end, '\n'));
+    return nl + (buf[end - 1] != '\n' ? 1 : 0);
+}
+
+// Split [begin, end) of buf into lines, written to out[0..count_lines).
+void scan_lines(const char* buf, size_t begin, size_t end, line_info* out) {
+    size_t pos = begin, k = 0;
     while (pos < end) {
         const char* nl = static_cast<const char*>(std::memchr(buf + pos, '\n', end - pos));
         const size_t le = nl ? static_cast<size_t>(nl - buf) : end;
@@ -116,7 +145,7 @@ void scan_lines(const char* buf, size_t begin, size_t end, std::vector<line_info
             const char* t2 = static_cast<const char*>(std::memchr(t1 + 1, '\t', le - li.tab - 1));
             li.tabs = t2 ? 2 : 1;
         }
-        out.push_back(li);
+        out[k++] = li;
         pos = le + 1;
     }
 }
@@ -130,6 +159,8 @@ int pf_dataset_load_tsv(pf_ctx* ctx, const char* data, size_t len, const char* s
     if (err) std::memset(err, 0, sizeof(*err));
     if (!out || (!data && len)) return PF_ERR_NULL_ARGUMENT;
     *out = nullptr;
+    (void)ctx;  // the loader runs on the host cores; kept for the ABI (pf_dataset_* take a ctx)
+    Trace tr;
     // ---- line scan, in parallel over newline-aligned chunks ----------------------
     const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::vector<size_t> cut(nt + 1, 0);
@@ -141,15 +172,24 @@ int pf_dataset_load_tsv(pf_ctx* ctx, const char* data, size_t len, const char* s
         cut[t] = nl ? static_cast<size_t>(nl - data) + 1 : len;
         if (cut[t] < cut[t - 1]) cut[t] = cut[t - 1];
     }
-    std::vector<std::vector<line_info>> parts(nt);
+    // two passes: count each chunk's lines, then fill one array at the offsets
+    std::vector<size_t> first(nt + 1, 0);
     {
         std::vector<std::thread> pool;
         for (unsigned t = 0; t < nt; ++t)
-            pool.emplace_back([&, t] { scan_lines(data, cut[t], cut[t + 1], parts[t]); });
+            pool.emplace_back([&, t] { first[t + 1] = count_lines(data, cut[t], cut[t + 1]); });
         for (auto& th : pool) th.join();
     }
-    std::vector<line_info> lines;
-    for (auto& p : parts) lines.insert(lines.end(), p.begin(), p.end());
+    for (unsigned t = 0; t < nt; ++t) first[t + 1] += first[t];
+    std::vector<line_info> lines(first[nt]);
+    {
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < nt; ++t)
+            pool.emplace_back(
+                [&, t] { scan_lines(data, cut[t], cut[t + 1], lines.data() + first[t]); });
+        for (auto& th : pool) th.join();
+    }
+    tr.mark("line scan");
 
     // ---- first structural problem (field count, empty field, lengths) ------------
     size_t ls = lines.size();  // index of the first line with a structural problem
@@ -165,10 +205,12 @@ int pf_dataset_load_tsv(pf_ctx* ctx, const char* data, size_t len, const char* s
     // ---- records of the well-formed prefix; bytes validated on the GPU ------------
     auto* ds = new pf_dataset;
     ds->source = source_name ? source_name : "<stream>";
+    tr.mark("structure check");
     if (!alloc_records(ds, ls, m)) {
         delete ds;
         return PF_ERR_OUT_OF_MEMORY;
     }
+    tr.mark("alloc records");
     {
         std::vector<std::thread> pool;
         for (unsigned t = 0; t < nt; ++t)
@@ -180,25 +222,22 @@ int pf_dataset_load_tsv(pf_ctx* ctx, const char* data, size_t len, const char* s
             });
         for (auto& th : pool) th.join();
     }
+    tr.mark("copy records");
     if (ls > 0) {
-        std::vector<uint32_t> acc((ls + 31) / 32);
-        pf_error verr{};
-        // e >= m: the filter only validates (shouji.cpp:48-49 short-circuit)
-        const int st = pf_shouji_filter_batch(ctx, ds->text, ds->pattern, m, ls, m, m, 4,
-                                              acc.data(), nullptr, nullptr, &verr);
-        if (st == PF_ERR_ILLEGAL_CHARACTER) {
-            const uint64_t line = verr.pair + 1;
-            const line_info& li = lines[verr.pair];
-            const char* f = data + (verr.field == 0 ? li.begin : li.tab + 1);
+        // the alphabet check of the well-formed prefix (the host pack's AVX-512
+        // check, exact first offender in pair order)
+        sb::HostBad bad;
+        sb::host_validate_parallel(ds->text, ds->pattern, m, static_cast<long long>(ls),
+                                   static_cast<int>(m), &bad);
+        if (bad.any) {
+            const uint64_t line = bad.pair + 1;
+            const line_info& li = lines[bad.pair];
+            const char* f = data + (bad.field == 0 ? li.begin : li.tab + 1);
             pf_dataset_free(ds);
             check_codec(f, m, line, err);  // same message the reference builds
             return PF_ERR_PARSE;
         }
-        if (st != PF_OK) {
-            pf_dataset_free(ds);
-            if (err) *err = verr;
-            return st;
-        }
+        tr.mark("validation");
     }
     if (ls < lines.size()) {  // the structural line, checked in the reference's order
         const line_info& li = lines[ls];
@@ -241,13 +280,44 @@ int pf_dataset_load_tsv(pf_ctx* ctx, const char* data, size_t len, const char* s
 int pf_dataset_load_tsv_file(pf_ctx* ctx, const char* path, pf_dataset** out, pf_error* err) {
     if (err) std::memset(err, 0, sizeof(*err));
     if (!path || !out) return PF_ERR_NULL_ARGUMENT;
-    std::ifstream f(path, std::ios::binary);
-    if (!f) {
+    Trace tr;
+    const int fd = open(path, O_RDONLY);
+    if (fd < 0) {
         set_parse(err, PF_ERR_PARSE, 0, std::string("cannot open pair file: ") + path);
         if (err) err->status = PF_ERR_PARSE;
         return PF_ERR_PARSE;
     }
-    std::string buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    struct stat st {};
+    if (fstat(fd, &st) == 0 && S_ISREG(st.st_mode) && st.st_size > 0) {
+        // a regular file is mapped, not copied: the loader's threads fault its
+        // pages in parallel while they scan it (a sized fread moved ~2 GB/s)
+        const size_t len = static_cast<size_t>(st.st_size);
+        void* map = mmap(nullptr, len, PROT_READ, MAP_PRIVATE, fd, 0);
+        close(fd);
+        if (map != MAP_FAILED) {
+            madvise(map, len, MADV_SEQUENTIAL);
+            tr.mark("file map");
+            const int rc = pf_dataset_load_tsv(ctx, static_cast<const char*>(map), len, path, out, err);
+            munmap(map, len);
+            return rc;
+        }
+        FILE* f = std::fopen(path, "rb");  // mapping refused: read it
+        if (!f) {
+            set_parse(err, PF_ERR_PARSE, 0, std::string("cannot open pair file: ") + path);
+            if (err) err->status = PF_ERR_PARSE;
+            return PF_ERR_PARSE;
+        }
+        std::string buf(len, '\0');
+        buf.resize(std::fread(buf.data(), 1, len, f));
+        std::fclose(f);
+        return pf_dataset_load_tsv(ctx, buf.data(), buf.size(), path, out, err);
+    }
+    // empty, a pipe or a special file: read it to the end
+    std::string buf;
+    char tmp[1 << 16];
+    for (ssize_t r; (r = read(fd, tmp, sizeof(tmp))) > 0;) buf.append(tmp, static_cast<size_t>(r));
+    close(fd);
+    tr.mark("file read");
     return pf_dataset_load_tsv(ctx, buf.data(), buf.size(), path, out, err);
 }
 

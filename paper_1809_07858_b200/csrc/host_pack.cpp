@@ -190,6 +190,30 @@ SB_AVX512 bool pack_dibit_rows_avx512(const uint8_t* text, const uint8_t* patter
     return anyn != 0;
 }
 
+// Rows [lo, hi): the byte check of pack_dibit_rows_avx512 without the packing.
+SB_AVX512 bool validate_rows_avx512(const uint8_t* text, const uint8_t* pattern, size_t stride,
+                                    int m, long long lo, long long hi) {
+    alignas(64) uint8_t lb[64];
+    for (int i = 0; i < 64; ++i) lb[i] = static_cast<uint8_t>(i ^ 1);
+    for (uint8_t c : {'A', 'C', 'G', 'N', 'T'}) lb[c & 63] = c;
+    const __m512i lut = _mm512_load_si512(lb);
+    __m512i acc = _mm512_setzero_si512();
+    for (long long r = lo; r < hi; ++r) {
+        if (r + kPrefetchRows < hi) prefetch_rows(text, pattern, stride, m, r + kPrefetchRows);
+        for (int f = 0; f < 2; ++f) {
+            const uint8_t* s = (f == 0 ? text : pattern) + r * stride;
+            for (int c0 = 0; c0 < m; c0 += 64) {
+                const int w = m - c0;
+                const __mmask64 k = w >= 64 ? ~0ull : ((1ull << w) - 1);
+                const __m512i v = _mm512_maskz_loadu_epi8(k, s + c0);
+                acc = _mm512_ternarylogic_epi32(acc, _mm512_maskz_permutexvar_epi8(k, v, lut), v,
+                                                0xF6);  // acc | (lut(v) ^ v)
+            }
+        }
+    }
+    return !_mm512_test_epi8_mask(acc, acc);
+}
+
 bool pack_dibit_rows_scalar(const uint8_t* text, const uint8_t* pattern, size_t stride, int m,
                             long long lo, long long hi, uint8_t* out_text, uint8_t* out_pattern,
                             uint8_t* n_text, uint8_t* n_pattern, HostBad* bad) {
@@ -353,6 +377,28 @@ void host_pack_nibbles_parallel(const uint8_t* text, const uint8_t* pattern, siz
     } else {
         pool().run(tasks, body);
     }
+    for (const auto& b : bads)
+        if (b.any) bad->offer(b.pair, b.field, b.pos, b.byte);
+}
+
+void host_validate_parallel(const uint8_t* text, const uint8_t* pattern, size_t stride,
+                            long long n, int m, HostBad* bad) {
+    if (n <= 0) return;
+    const bool simd = has_avx512();
+    const unsigned nt = host_pack_threads();
+    const size_t tasks = static_cast<size_t>(std::max<long long>(
+        1, std::min<long long>((n + 1023) / 1024, 4ll * nt)));
+    std::vector<HostBad> bads(tasks);
+    auto body = [&](size_t t) {
+        const long long lo = n * static_cast<long long>(t) / static_cast<long long>(tasks);
+        const long long hi = n * static_cast<long long>(t + 1) / static_cast<long long>(tasks);
+        if (!simd || !validate_rows_avx512(text, pattern, stride, m, lo, hi))
+            scan_bad(text, pattern, stride, m, lo, hi, &bads[t]);
+    };
+    if (tasks == 1)
+        body(0);
+    else
+        pool().run(tasks, body);
     for (const auto& b : bads)
         if (b.any) bad->offer(b.pair, b.field, b.pos, b.byte);
 }

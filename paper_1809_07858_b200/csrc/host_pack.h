@@ -46,6 +46,11 @@ void host_pack_dibits_parallel(const uint8_t* text, const uint8_t* pattern, size
                                uint8_t* n_text, uint8_t* n_pattern, HostBad* bad, bool* has_n,
                                bool allow_simd = true);
 
+// Alphabet check only (packed_sequence::from_string's byte rule) over n pairs
+// on the worker pool: bad receives the first illegal byte in pair order.
+void host_validate_parallel(const uint8_t* text, const uint8_t* pattern, size_t stride,
+                            long long n, int m, HostBad* bad);
+
 // memcpy on the same worker pool (pageable -> pinned staging copies).
 void host_copy_parallel(void* dst, const void* src, size_t bytes);
 

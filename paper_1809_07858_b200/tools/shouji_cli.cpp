@@ -23,6 +23,7 @@
 #include <optional>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "shouji_b200.h"
@@ -159,15 +160,35 @@ uint32_t resolve_threshold(const options& o, size_t m) {
 
 // --pairs FILE / - or the generator; the threshold needs m, and the generator's
 // default edit range 0..2e needs the threshold (cli.cpp:96-110).
+// The CUDA context (driver init, ~1 s) is created on a helper thread while the
+// host cores load or generate the pairs; the filter calls that follow use it.
+struct ctx_init {
+    ctx_holder& ch;
+    std::thread t;
+    explicit ctx_init(ctx_holder& c) : ch(c), t([this] {
+        try {
+            ch.get();
+        } catch (...) {  // reported by the next ch.get() on the main thread
+        }
+    }) {}
+    ~ctx_init() { t.join(); }
+};
+
 uint32_t resolve_input(const options& o, ctx_holder& ch, dataset_holder& dh) {
     pf_error err{};
     if (!o.pairs_file.empty()) {
-        if (o.pairs_file == "-") {
-            std::string buf((std::istreambuf_iterator<char>(std::cin)), std::istreambuf_iterator<char>());
-            check(pf_dataset_load_tsv(ch.get(), buf.data(), buf.size(), "<stdin>", &dh.ds, &err), err);
-        } else {
-            check(pf_dataset_load_tsv_file(ch.get(), o.pairs_file.c_str(), &dh.ds, &err), err);
+        int st;
+        {
+            ctx_init init(ch);
+            if (o.pairs_file == "-") {
+                std::string buf((std::istreambuf_iterator<char>(std::cin)),
+                                std::istreambuf_iterator<char>());
+                st = pf_dataset_load_tsv(nullptr, buf.data(), buf.size(), "<stdin>", &dh.ds, &err);
+            } else {
+                st = pf_dataset_load_tsv_file(nullptr, o.pairs_file.c_str(), &dh.ds, &err);
+            }
         }
+        check(st, err);
         return resolve_threshold(o, pf_dataset_length(dh.ds));
     }
     const uint32_t len = o.len.empty() ? 0 : parse_u32(o.len, "--len");
@@ -175,7 +196,12 @@ uint32_t resolve_input(const options& o, ctx_holder& ch, dataset_holder& dh) {
     const uint32_t e = resolve_threshold(o, len);
     const uint32_t dhi = static_cast<uint32_t>(std::min<uint64_t>(2 * uint64_t(e), len));
     const auto ed = o.edits.empty() ? std::make_pair(0u, dhi) : parse_edits(o.edits);
-    check(pf_dataset_generate(o.seed, o.count, len, ed.first, ed.second, &dh.ds, &err), err);
+    int st;
+    {
+        ctx_init init(ch);
+        st = pf_dataset_generate(o.seed, o.count, len, ed.first, ed.second, &dh.ds, &err);
+    }
+    check(st, err);
     return e;
 }
 
