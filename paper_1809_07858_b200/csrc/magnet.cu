@@ -435,8 +435,11 @@ __device__ __forceinline__ void diag_vector(int d, const uint32_t (&Plo)[W], con
     }
 }
 
+// Up to 256 columns: 4 CTAs (16 warps) per SM at 128 registers (ptxas would
+// take 168-190 and fit 2-3; the few spills cost less than the lost warps):
+// m=150 E=15 83 -> 109, m=250 E=15 68 -> 90, E=25 37.6 -> 50.8 M pairs/s.
 template <int W, class Src>
-__global__ void __launch_bounds__(kMagnetWarpNT)
+__global__ void __launch_bounds__(kMagnetWarpNT, (W <= 8 ? 4 : 1))
 magnet_warp_kernel(Src src, long long n, int m, int e, uint32_t* __restrict__ accept,
                    uint32_t* __restrict__ estimates, uint64_t* __restrict__ bits) {
     constexpr int kStack = 16 * W + 4;
