@@ -99,12 +99,16 @@ __device__ __forceinline__ uint32_t fsm_step4(const Cand4& best, uint32_t (&S)[3
 
 template <int E>
 struct SearchCfg {
+    // measured: the carried form at 8 <= E <= 12 beats the rebuilding form
+    // (4 CTAs/SM) by 3-6% despite its register pressure
     static constexpr bool CARRY = E <= 12;
     static constexpr int B = 4;  // windows per block
     static constexpr int NT = 128;
     // 4 CTAs (16 warps) per SM where the carried D columns still fit 128
-    // registers without spilling (E <= 7); larger E keeps the compiler's choice.
-    static constexpr int MINB = E <= 7 ? 4 : 1;
+    // registers without spilling (E <= 7); 3 CTAs for 8 <= E <= 12 (168
+    // registers instead of 190-242 at 2 CTAs: +2-3.5%; 4 CTAs spill and lose);
+    // the rebuilding form (E > 12) fits 4 CTAs on its own.
+    static constexpr int MINB = E <= 7 ? 4 : (E <= 12 ? 3 : 1);
 };
 
 // Column loads relative to per-block base pointers: lo/hi word (x*2 + k) * 8
