@@ -247,10 +247,11 @@ struct DibitSrc {
 };
 
 // Up to 128 columns: 4 CTAs (16 warps) per SM at 128 registers (ptxas would
-// take 141 and fit 3): m=100 E=2/5/10 +15-17%. Longer records keep the
-// compiler's choice (they already spill at their natural size).
+// take 141 and fit 3): m=100 E=2/5/10 +15-17%. 129-256 columns: 3 CTAs at 168
+// (from 255 + spills at 2): m=150 E=7 +5%, m=250 E=10 +10%, E<=5 within 1%.
+// Longer records keep the compiler's choice.
 template <int W, class Src>
-__global__ void __launch_bounds__(128, (W <= 4 ? 4 : 1))
+__global__ void __launch_bounds__(128, (W <= 4 ? 4 : (W <= 8 ? 3 : 1)))
 magnet_kernel(Src src, long long n, int m, int e, uint32_t* __restrict__ accept,
               uint32_t* __restrict__ estimates, uint64_t* __restrict__ bits) {
     const long long pair = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
