@@ -64,3 +64,62 @@ def test_cli_data_error_exit_2(tmp_path):
     assert rc == 1  # cannot plant more edits than bases: invalid parameters
     rc, _, err = run("filter", "--pairs", str(tmp_path / "missing.tsv"), "--e", "1")
     assert rc == 2 and b"error" in err
+
+
+# --- TSV ingest on the host cores (pf_dataset_load_tsv_file; no CUDA context) -------
+
+def _load_file(path):
+    import ctypes as C
+    from paper_1809_07858_b200 import _lib as L
+    h = C.c_void_p()
+    err = L.PfError()
+    st = L.lib.pf_dataset_load_tsv_file(None, str(path).encode(), C.byref(h), C.byref(err))
+    if st != L.PF_OK:
+        return st, err, None
+    n, m = L.lib.pf_dataset_size(h), L.lib.pf_dataset_length(h)
+    t = np.frombuffer((C.c_uint8 * (n * m)).from_address(L.lib.pf_dataset_text(h)), np.uint8).reshape(n, m).copy()
+    p = np.frombuffer((C.c_uint8 * (n * m)).from_address(L.lib.pf_dataset_pattern(h)), np.uint8).reshape(n, m).copy()
+    L.lib.pf_dataset_free(h)
+    return st, err, (t, p)
+
+
+def test_load_tsv_file_roundtrip_and_edges(oracle, tmp_path):
+    # load_pairs_file (dataset.cpp:13-44): mmap'd regular file, getline line semantics
+    t, p = oracle.generate_pairs(11, 5000, 100, 0, 10)
+    body = b"".join(t[i].tobytes() + b"\t" + p[i].tobytes() + b"\n" for i in range(len(t)))
+    f = tmp_path / "pairs.tsv"
+    f.write_bytes(body)
+    st, _, rec = _load_file(f)
+    assert st == 0 and (rec[0] == t).all() and (rec[1] == p).all()
+    f.write_bytes(body[:-1])  # no trailing newline: the last line still counts
+    st, _, rec = _load_file(f)
+    assert st == 0 and rec[0].shape == (5000, 100) and (rec[1] == p).all()
+    f.write_bytes(b"")  # empty input
+    st, err, _ = _load_file(f)
+    assert st != 0 and err.line == 1 and b"no pairs in input" in bytes(err.message)
+    bad = bytearray(body)
+    bad[3 * 202 + 101 + 17] = ord("x")  # line 4, pattern position 17
+    f.write_bytes(bytes(bad))
+    st, err, _ = _load_file(f)
+    assert st != 0 and err.line == 4 and err.position == 17 and err.byte == ord("x")
+    assert b"illegal character 'x' at position 17" in bytes(err.message)
+    extra = body[:202 * 7] + t[7].tobytes() + b"\t" + p[7].tobytes() + b"\tX\n"
+    f.write_bytes(extra)
+    st, err, _ = _load_file(f)
+    assert st != 0 and err.line == 8 and b"found more" in bytes(err.message)
+    st, err, _ = _load_file(tmp_path / "missing.tsv")
+    assert st != 0 and b"cannot open pair file" in bytes(err.message)
+
+
+def test_load_tsv_from_a_fifo(oracle, tmp_path):
+    # a non-regular file (named pipe) is read to its end instead of mapped
+    import threading
+    t, p = oracle.generate_pairs(12, 300, 50, 0, 5)
+    body = b"".join(t[i].tobytes() + b"\t" + p[i].tobytes() + b"\n" for i in range(len(t)))
+    fifo = tmp_path / "pairs.fifo"
+    os.mkfifo(fifo)
+    w = threading.Thread(target=lambda: fifo.write_bytes(body))
+    w.start()
+    st, _, rec = _load_file(fifo)
+    w.join()
+    assert st == 0 and (rec[0] == t).all() and (rec[1] == p).all()
