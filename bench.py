@@ -140,6 +140,26 @@ class ClockSampler:
                                     if p[3].replace(".", "").isdigit()), default=None)}
 
 
+SEED0 = 1809078581  # tests/golden/make_fullsize_digests.py seeds configs[1] at E the same way
+
+
+def workload_seed(e: int, rank: int) -> int:
+    """Rank 0's shard is the configs[1] set whose full-size digests are pinned in
+    tests/golden/fullsize_digests.json (seed SEED0 + 1000 E)."""
+    return SEED0 + 1000 * e + 7919 * rank
+
+
+def workload_config(n, m, e, world):
+    """The `config` object of both arms (identical, so the driver compares like with like)."""
+    pitch = ((m + 3) // 4) * 4
+    return {"workload": f"configs[1] m={m} E={e}: {n} pairs per GPU, 50% planted "
+                        f"k~U{{0..{2 * e}}} sub/ins/del, 50% independent; ASCII records, pitch {pitch}",
+            "m": m, "E": e, "width": 4, "pairs_per_gpu": n, "global_pairs": n * world,
+            "seed": workload_seed(e, 0),
+            "parallelism": f"dp{world} (contiguous pair shards, no collective)",
+            "l2": f"inputs {2 * n * pitch / 1e9:.1f} GB per GPU >> 126 MB L2 (no flush)"}
+
+
 # ------------------------------------------------------------------------------------
 # CPU baseline: the unmodified reference library on this host's cores
 # ------------------------------------------------------------------------------------
@@ -196,37 +216,26 @@ def cpu_baseline(text, pattern, e, target_s, threads=None):
     return out
 
 
-def reference_workload(n, m, e, seed):
-    """CPU-generated sample of BASELINE configs[1] at E: even pairs planted by the
-    reference generator (k ~ U{0..2E}, dataset.cpp:71-126), odd pairs independent."""
-    from oracle.oracle import Oracle, Reference
-    gen = Reference() if Reference.available() else Oracle()
-    half = (n + 1) // 2
-    t_pl, p_pl = gen.generate_pairs(seed, half, m, 0, min(2 * e, m))
-    rng = np.random.default_rng(seed)
-    alpha = np.frombuffer(b"ACGT", np.uint8)
-    t = np.empty((n, m), np.uint8)
-    p = np.empty((n, m), np.uint8)
-    t[0::2], p[0::2] = t_pl[: (n + 1) // 2], p_pl[: (n + 1) // 2]
-    t[1::2] = alpha[rng.integers(0, 4, size=(n // 2, m))]
-    p[1::2] = alpha[rng.integers(0, 4, size=(n // 2, m))]
-    return t, p
-
-
 def run_reference_arm(args, rank, world):
+    """The reference library (oracle/_ref, compiled unmodified from its sources) on the
+    host cores, over a bounded prefix of the SAME bytes our arm filters (configs[1] at
+    E, rank 0's shard: the CPU mirror of the device generator, oracle/config_oracle.c,
+    reproduces them byte for byte), under the same `config` object."""
     if rank != 0:
         return
     from oracle.oracle import Oracle, Reference
     kind = "reference" if Reference.available() else "port"
-    lib = Reference() if kind == "reference" else Oracle()
+    gen = Oracle()
+    lib = Reference() if kind == "reference" else gen
     threads = lib.hardware_concurrency() if kind == "reference" else (os.cpu_count() or 1)
+    seed = workload_seed(args.e, 0)
     # bounded sample per step: ~2.5 s of CPU work per step
-    t, p = reference_workload(40_000, args.m, args.e, 1809078581 + 1000 * args.e)
+    t, p = gen.gen_config(1, seed, args.e, args.m, 0, 40_000)
     t0 = time.perf_counter()
     lib.shouji_batch(t, p, args.e, threads=threads, estimates=False)
     rate = t.shape[0] / max(time.perf_counter() - t0, 1e-6)
-    n = int(min(4_000_000, max(40_000, rate * 2.5)))
-    t, p = reference_workload(n, args.m, args.e, 1809078581 + 1000 * args.e)
+    n = int(min(args.pairs, 4_000_000, max(40_000, rate * 2.5))) // 32 * 32
+    t, p = gen.gen_config(1, seed, args.e, args.m, 0, n)
     packed = lib.pack(t, p) if kind == "reference" else None
     run = (lambda: packed.shouji(args.e, threads=threads, estimates=False)) if packed else \
         (lambda: lib.shouji_batch(t, p, args.e, threads=threads, estimates=False))
@@ -241,18 +250,18 @@ def run_reference_arm(args, rank, world):
         packed.free()
     total = sum(times)
     value = n * args.steps / total
+    sample = (f"first {n} pairs of rank 0's configs[1] shard (seed {seed}; the same bytes the "
+              f"device arm filters, regenerated by the CPU mirror of csrc/datagen.cu) per step, "
+              f"pre-packed (packing excluded, as run_bench, bench.cpp:24-25), parallel_for_pairs "
+              f"with {threads} threads, CPU: {lscpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (CPU-generated sample of BASELINE configs[1] at E=5)",
-        "config": {"workload": f"configs[1] m={args.m} E={args.e}: bounded sample of {n} pairs "
-                               f"per step on the host CPU", "m": args.m, "E": args.e,
-                   "pairs_per_step": n},
+        "data": "synthetic (BASELINE configs[1] at E=5, seeded; CPU-regenerated prefix)",
+        "config": workload_config(args.pairs, args.m, args.e, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(threads), "kind": kind,
-                         "sample": f"{n} pairs per step (50% planted k~U{{0..{2 * args.e}}} by the "
-                                   f"reference generator, 50% independent), pre-packed, "
-                                   f"parallel_for_pairs with {threads} threads, CPU: {lscpu_model()}"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -278,6 +287,123 @@ def reduce_max(values, dev, world):
     return [float(x) for x in t.cpu()]
 
 
+def load_profile(name):
+    path = os.path.join(ROOT, "profiles", name)
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def build_roofline(pf, ctx, dev, rank, n, m, e, pitch, step_ms, kern_avg_ms, stage_ms, peaks,
+                   peak_src, value_per_gpu):
+    """The contract's roofline object and the INT view beside it.
+
+    Algorithmic bytes are SURVEY.md §8(d)'s B(m) = 2m ASCII in + 1/8 accept bit out per pair
+    (200.125 B at m=100), for the dominant kernel (achieved = B x pairs / its live-measured
+    launch time) and for the whole step (``step``). ``traffic`` is ncu DRAM bytes per launch
+    (profiles/traffic.json). ``alu_overlap_bound`` is the step's ceiling if pack and search
+    overlapped perfectly: max(HBM time of B, summed ALU-pipe busy time of both kernels at
+    100%) per pair, the ALU time from ncu (profiles/alu.json: ncu sm__inst_executed_pipe_alu
+    warp instructions per kernel x 32 lanes at the measured LOP3 rate); ``serial_floor`` is the two kernels back to back, each at its peak.
+    """
+    import torch
+    hbm = float(peaks["hbm_gbs"])
+    B = 2 * m + 1 / 8
+    nflags = os.environ.get("PF_NFLAGS", "1") != "0"
+    tj = load_profile("traffic.json") or {}
+    scale = n / float(tj["pairs"]) if tj.get("pairs") else None
+    traffic_step = float(tj["dram_bytes_per_launch"]) * scale if scale else None
+    kb = tj.get("per_kernel_bytes", {}) if scale else {}
+    pack_traffic = float(kb["pack_tile_kernel"]) * scale if "pack_tile_kernel" in kb else None
+    search_traffic = float(kb["shouji_search_w4"]) * scale if "shouji_search_w4" in kb else None
+    src = f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"
+    step = {"bound": "hbm", "achieved": B * n / (kern_avg_ms * 1e-3) / 1e9, "peak": hbm,
+            "unit": "GB/s", "frac": B * n / (kern_avg_ms * 1e-3) / 1e9 / hbm,
+            "traffic": traffic_step, "algorithmic_bytes_per_pair": B, "kernel_ms_avg": kern_avg_ms,
+            "what": "whole step (pack + search launches), SURVEY 8(d) bytes over the step time"}
+    roofline = dict(step)
+    roofline["peak_source"] = src
+    per_kernel = None
+    lop3 = None
+    if rank == 0:
+        try:
+            lop3 = pf.int_peak("lop3", ctx=ctx)
+        except Exception:
+            lop3 = None
+    if stage_ms is not None:
+        pk_ms, se_ms = stage_ms
+        # the pack's own traffic: ASCII in; lo/hi planes x 2 sequences out (+ N planes
+        # unless skipped for N-free pair blocks)
+        pack_bytes = 2 * m + 2 * 2 * m / 8 + (0 if nflags else 2 * m / 8)
+        windows = ((m + 3 + 3) // 4) * 4
+        lop3_pair = ((2 * e + 1) * (6 if nflags else 7) + 2 * e * 10 + 19) * windows / 32
+        per_kernel = [
+            {"kernel": f"sb::pack_tile_kernel<8,128,{(pitch // 4) % 4},0,1>", "ms": pk_ms,
+             "share": pk_ms / (pk_ms + se_ms), "bound": "hbm",
+             "algorithmic_bytes_per_pair": B,
+             "achieved": B * n / (pk_ms * 1e-3) / 1e9, "unit": "GB/s",
+             "frac": B * n / (pk_ms * 1e-3) / 1e9 / hbm, "traffic": pack_traffic,
+             "moved_bytes_per_pair": pack_bytes,
+             "moved_frac": pack_bytes * n / (pk_ms * 1e-3) / 1e9 / hbm},
+            {"kernel": f"sb::shouji_search_w4<{e}>", "ms": se_ms, "share": se_ms / (pk_ms + se_ms),
+             "bound": "int (ALU pipe, LOP3)", "algorithmic_lop3_per_pair": lop3_pair,
+             "achieved": lop3_pair * n / (se_ms * 1e-3), "unit": "lane-ops/s",
+             "traffic": search_traffic},
+        ]
+        if lop3:
+            per_kernel[1]["peak"] = lop3
+            per_kernel[1]["frac"] = per_kernel[1]["achieved"] / lop3
+        dom = per_kernel[0] if pk_ms >= se_ms else per_kernel[1]
+        if dom is per_kernel[0]:
+            roofline = {"bound": "hbm", "achieved": dom["achieved"], "peak": hbm, "unit": "GB/s",
+                        "frac": dom["frac"], "traffic": pack_traffic, "peak_source": src,
+                        "kernel": dom["kernel"], "share_of_step": dom["share"],
+                        "algorithmic_bytes_per_pair": B, "kernel_ms_avg": pk_ms,
+                        "what": "dominant kernel (pack): SURVEY 8(d) bytes per pair x pairs / "
+                                "its launch time (CUDA events between the two launches)"}
+        roofline["step"] = step
+        roofline["per_kernel"] = per_kernel
+        if lop3:
+            roofline["serial_floor"] = {
+                "pairs_per_s_per_gpu": 1.0 / (pack_bytes / (hbm * 1e9) + lop3_pair / lop3),
+                "frac": value_per_gpu * (pack_bytes / (hbm * 1e9) + lop3_pair / lop3),
+                "what": "pack moving its bytes at the HBM peak + search at the measured LOP3 "
+                        "peak, back to back"}
+    alu = load_profile("alu.json")
+    if alu and alu.get("pairs") and lop3:
+        # ALU-pipe lane-ops per pair of both kernels (ncu sm__inst_executed_pipe_alu x 32)
+        # at the measured LOP3 lane rate of this GPU
+        lanes = sum(k["inst_executed_pipe_alu"] for k in alu["kernels"].values()) * 32.0
+        alu_s = lanes / float(alu["pairs"]) / lop3
+        hbm_s = B / (hbm * 1e9)
+        bound = 1.0 / max(alu_s, hbm_s)
+        roofline["alu_overlap_bound"] = {
+            "pairs_per_s_per_gpu": bound, "frac": value_per_gpu / bound,
+            "binding": "alu" if alu_s > hbm_s else "hbm",
+            "alu_ps_per_pair": alu_s * 1e12, "hbm_ps_per_pair": hbm_s * 1e12,
+            "alu_lane_ops_per_pair": lanes / float(alu["pairs"]),
+            "source": "profiles/alu.json (" + alu.get("source", "ncu") + ")",
+            "what": "max(HBM time of 2m+1/8 B, summed ALU-pipe busy time of pack + search at "
+                    "100% of the pipe) per pair: the ceiling of any overlap of the two stages"}
+    int_view = None
+    if rank == 0 and lop3:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ops_pair = 25 * (2 * e + 1) * ((m + 31) // 32) + 8 * m  # BASELINE.md OPS(m,E)
+        int_bound = lop3 / ops_pair
+        int_view = {"ops_per_pair_formula": ops_pair, "lop3_lane_ops_per_s": lop3,
+                    "lop3_lanes_per_clk_per_sm_at_max_clock":
+                        lop3 / (sms * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6),
+                    "int_bound_pairs_per_s_per_gpu": int_bound,
+                    "frac_of_int_bound": value_per_gpu / int_bound,
+                    "hbm_bound_pairs_per_s_per_gpu": hbm * 1e9 / B,
+                    "note": "BASELINE.md's frozen OPS formula counts 1900 ops/pair; the kernels "
+                            "execute fewer (ncu), so this is not a ceiling for this design - "
+                            "alu_overlap_bound is"}
+    return roofline, int_view
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -298,7 +424,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- workload: configs[1] at E on this rank's device ---------------------------
     text = torch.empty((n, pitch), dtype=torch.uint8, device=dev)
     pattern = torch.empty((n, pitch), dtype=torch.uint8, device=dev)
-    seed = 1809078581 + 1000 * e + 7919 * rank
+    seed = workload_seed(e, rank)
     pf.generate_device(1, seed, e, text.data_ptr(), pattern.data_ptr(), pitch, n, m, stream=sh,
                        ctx=ctx)
     accept = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev)
@@ -397,6 +523,9 @@ def run_ours(args, rank, world, local_rank):
         t_e2e = (t_e2e0, time.perf_counter())
         x1 = pf.transfer_bytes()
         assert (acc_h[: chk // 32] == a_ref).all()
+        # the host path reads every record byte once (2m B/pair): the host cores'
+        # stream-read rate over these same pinned records bounds it (outside the clock)
+        host_gbs = pf.host_read_bandwidth(tn, passes=2)
         e2e_s = reduce_max([sum(tw) / len(tw)], dev, world)[0]
         e2e = {"value": world * n / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": (x1[0] - x0[0]) // args.steps,
@@ -404,6 +533,11 @@ def run_ours(args, rank, world, local_rank):
                "ascii_bytes_per_step": int(2 * n * m),
                "ms_per_step": 1e3 * e2e_s,
                "step_ms": [round(1e3 * x, 2) for x in tw],
+               "host_read_gbs": host_gbs,
+               "host_threads": int(os.environ.get("PF_HOST_THREADS", os.cpu_count() or 1)),
+               "host_bound_pairs_per_s": host_gbs * 1e9 / (2 * m),
+               "frac_of_host_bound": (world * n / e2e_s) / (host_gbs * 1e9 / (2 * m))
+               if host_gbs > 0 else None,
                "path": "pf_shouji_filter_batch(pinned host ASCII records, stride=m): host cores pack "
                        "2-bit dibit records (N planes only for chunks with an N) chunk by chunk into "
                        "pinned buffers, H2D, device pack + search kernels, D2H accept bitmap, sync"
@@ -420,100 +554,8 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- roofline -----------------------------------------------------------------------
     peaks, peak_src = measured_peaks()
-    alg_bytes = n * (2 * m + 1 / 8)  # ASCII text+pattern in, one accept bit out
-    achieved_gbs = alg_bytes / (kern_avg_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            tj = json.load(open(tpath))
-            if tj.get("pairs") and tj.get("dram_bytes_per_launch"):
-                traffic = float(tj["dram_bytes_per_launch"]) * n / float(tj["pairs"])
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": float(peaks["hbm_gbs"]),
-                "unit": "GB/s", "frac": achieved_gbs / float(peaks["hbm_gbs"]), "traffic": traffic,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
-                "algorithmic_bytes_per_pair": 2 * m + 1 / 8,
-                "kernels": "sb::pack_tile_kernel (TMA records -> planes, validation) + "
-                           "sb::shouji_search_w4<5> (map+search+commit+accept); achieved is over "
-                           "the whole step (both launches)",
-                "kernel_ms_avg": kern_avg_ms}
-    if stage_ms is not None:
-        pk_ms, se_ms = stage_ms
-        pack_traffic = None
-        try:
-            tj = json.load(open(tpath))
-            pack_traffic = float(tj["per_kernel_bytes"]["pack_tile_kernel"]) * n / float(tj["pairs"])
-            search_traffic = float(tj["per_kernel_bytes"]["shouji_search_w4"]) * n / float(tj["pairs"])
-        except Exception:
-            pack_traffic = search_traffic = None
-        # ASCII in; lo/hi planes x 2 sequences out, plus the N planes unless the pack
-        # skips them (N-presence flags, pack.cuh: the synthetic config-1 data has no N)
-        nflags = os.environ.get("PF_NFLAGS", "1") != "0"
-        pack_bytes = n * (2 * m + 2 * 2 * m / 8 + (0 if nflags else 2 * m / 8))
-        # algorithmic LOP3 of the search per 32-pair group and window: map 2 (N-free
-        # warps; 3 with N planes) + key 4 per diagonal (two windows share a 3-column
-        # popcount), compare 4 + mux 6 per diagonal after the first, commit FSM (incl.
-        # recovering the unselected slice bit) + tally 19
-        windows = ((m + 3 + 3) // 4) * 4
-        lop3_pair = ((2 * e + 1) * (6 if nflags else 7) + 2 * e * 10 + 19) * windows / 32
-        roofline["per_kernel"] = [
-            {"kernel": f"sb::pack_tile_kernel<8,128,{(pitch // 4) % 4},0,1>", "ms": pk_ms, "share": pk_ms / (pk_ms + se_ms),
-             "bound": "hbm", "algorithmic_bytes_per_pair": pack_bytes / n,
-             "achieved": pack_bytes / (pk_ms * 1e-3) / 1e9, "unit": "GB/s",
-             "frac": pack_bytes / (pk_ms * 1e-3) / 1e9 / float(peaks["hbm_gbs"]),
-             "traffic": pack_traffic},
-            {"kernel": f"sb::shouji_search_w4<{e}>", "ms": se_ms, "share": se_ms / (pk_ms + se_ms),
-             "bound": "int (ALU pipe, LOP3)", "algorithmic_lop3_per_pair": lop3_pair,
-             "achieved": lop3_pair * n / (se_ms * 1e-3), "unit": "lane-ops/s",
-             "traffic": search_traffic},
-        ]
-    int_view = None
-    if rank == 0:
-        try:
-            lop3 = pf.int_peak("lop3", ctx=ctx)
-            sms = torch.cuda.get_device_properties(dev).multi_processor_count
-            ops_pair = 25 * (2 * e + 1) * ((m + 31) // 32) + 8 * m  # BASELINE.md OPS(m,E)
-            int_bound = lop3 / ops_pair
-            if "per_kernel" in roofline:
-                sk = roofline["per_kernel"][1]
-                sk["peak"] = lop3
-                sk["frac"] = sk["achieved"] / lop3
-                # the design's own floor: pack at the HBM peak (its algorithmic bytes)
-                # plus search at the LOP3 peak (its algorithmic LOP3), run back to back
-                pk0 = roofline["per_kernel"][0]
-                floor_s = (pk0["algorithmic_bytes_per_pair"] / (float(peaks["hbm_gbs"]) * 1e9)
-                           + sk["algorithmic_lop3_per_pair"] / lop3)
-                roofline["design_floor"] = {
-                    "pairs_per_s_per_gpu": 1.0 / floor_s,
-                    "frac": (value / world) * floor_s,
-                    "what": "pack kernel at the measured HBM peak + search kernel at the measured "
-                            "LOP3 peak, per pair, back to back"}
-            int_view = {"ops_per_pair_formula": ops_pair, "lop3_lane_ops_per_s": lop3,
-                        "lop3_lanes_per_clk_per_sm_at_max_clock":
-                            lop3 / (sms * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6),
-                        "int_bound_pairs_per_s_per_gpu": int_bound,
-                        "frac_of_int_bound": (value / world) / int_bound,
-                        "hbm_bound_pairs_per_s_per_gpu":
-                            float(peaks["hbm_gbs"]) * 1e9 / (2 * m + 1 / 8)}
-        except Exception as ex:  # diagnostic only
-            int_view = {"error": str(ex)}
-
-    # The contract's roofline is the DOMINANT kernel's: when the pack kernel (HBM-bound)
-    # takes the larger share of the step it becomes the top-level object; the whole-step
-    # view is kept under "step".
-    if "per_kernel" in roofline:
-        pk = roofline["per_kernel"][0]
-        if pk["share"] >= 0.5:
-            step_view = {k: v for k, v in roofline.items() if k not in ("per_kernel", "design_floor")}
-            roofline = {"bound": "hbm", "achieved": pk["achieved"], "peak": float(peaks["hbm_gbs"]),
-                        "unit": "GB/s", "frac": pk["frac"], "traffic": pk["traffic"],
-                        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
-                        "kernel": pk["kernel"], "share_of_step": pk["share"],
-                        "algorithmic_bytes_per_pair": pk["algorithmic_bytes_per_pair"],
-                        "kernel_ms_avg": pk["ms"], "per_kernel": roofline["per_kernel"],
-                        "design_floor": roofline.get("design_floor"), "step": step_view}
+    roofline, int_view = build_roofline(pf, ctx, dev, rank, n, m, e, pitch, step_ms, kern_avg_ms,
+                                        stage_ms, peaks, peak_src, value / world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -536,12 +578,7 @@ def run_ours(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (device-generated BASELINE configs[1] at E=5; seeded)",
-            "config": {"workload": f"configs[1] m={m} E={e}: {n} pairs per GPU, 50% planted "
-                                   f"k~U{{0..{2 * e}}} sub/ins/del, 50% independent; ASCII records, "
-                                   f"pitch {pitch}", "m": m, "E": e, "width": 4,
-                       "pairs_per_gpu": n, "global_pairs": n * world,
-                       "parallelism": f"dp{world} (contiguous pair shards, no collective)",
-                       "l2": f"inputs {2 * n * pitch / 1e9:.1f} GB per GPU >> 126 MB L2 (no flush)"},
+            "config": workload_config(n, m, e, world),
             "roofline": roofline, "int_roofline": int_view, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": ck, "clocks_e2e": ck_e2e,
             "kernel_ms": [round(x, 4) for x in kern_ms],
@@ -550,8 +587,26 @@ def run_ours(args, rank, world, local_rank):
     ctx.close()
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     args = parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "reference":
+            # the reference arm runs on rank 0's host cores only: no ranks to spawn
+            run_reference_arm(args, 0, args.gpus)
+            return
+        # `bench.py --gpus N` outside torchrun: one rank per GPU, launched the way the
+        # driver launches it (torch.distributed.run, 127.0.0.1 rendezvous)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -106,7 +106,9 @@ int pf_shouji_filter_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* patt
  * on `stream` (a cudaStream_t; NULL = the legacy default stream) except that an error
  * check forces a stream synchronisation at the end. Records need a pitch that
  * is a multiple of 4 and >= m (pf_device_pitch(m) = round4(m) is the tight
- * layout) and 16-byte aligned bases; bytes in [m, pitch) are ignored. Output pointers
+ * layout) and 16-byte aligned bases; bytes in [m, pitch) are ignored, but they are
+ * read: each record array must span n*pitch bytes (the last record included; its
+ * padding is loaded by the tile copies and never used). Output pointers
  * are device pointers (accept_bitmap ceil(n/32) words; estimates/bits as for
  * the host call, may be NULL). */
 int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d_pattern,
@@ -292,6 +294,13 @@ uint64_t pf_launch_count(void);
  * (pf_shouji_filter_batch and friends) so far in this process; bench.py
  * reports the per-step delta as the e2e transfer volume. Either may be NULL. */
 void pf_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
+
+/* Diagnostic: how fast this host's cores stream-read `bytes` of the caller's
+ * buffer (GB/s; the host pack's AVX-512 loads and prefetch, all pool threads,
+ * `passes` timed passes after a warm one). Every host entry point must read
+ * each record byte once, so this is the ceiling of the host-records e2e path:
+ * pairs/s <= gbs * 1e9 / (2 * m). Returns 0 for buffers under 1 MiB. No GPU. */
+double pf_host_read_bandwidth(const void* buf, size_t bytes, int passes);
 
 #ifdef __cplusplus
 }

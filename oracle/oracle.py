@@ -80,6 +80,18 @@ class Oracle:
         lib.so_recover_subsequences.restype = C.c_size_t
         lib.so_longest_zero_run.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t,
                                             C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
+        # config_oracle.c: generator mirror of csrc/datagen.cu + vectorisable restatement
+        lib.so_gen_config.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_int, C.c_uint64,
+                                      C.c_size_t, C.c_void_p, C.c_void_p, C.c_size_t]
+        lib.so_gen_config_rows.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_int, C.c_void_p,
+                                           C.c_size_t, C.c_void_p, C.c_void_p, C.c_size_t]
+        lib.so_shouji_fast_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t,
+                                             C.c_int, C.c_uint32, C.c_uint, C.c_uint, C.c_void_p]
+        lib.so_config_estimates.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_int, C.c_uint32,
+                                            C.c_uint, C.c_uint64, C.c_size_t, C.c_uint,
+                                            C.c_void_p]
+        lib.so_shouji_fast_one.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_uint32, C.c_uint,
+                                           C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_int)]
         self.lib = lib
 
     def set_variant(self, v: int):
@@ -101,6 +113,48 @@ class Oracle:
         if st:
             raise OracleError(st, err.pair, err.field, err.position, err.byte)
         return acc, est, bv
+
+    # ---- config_oracle.c -----------------------------------------------------------
+    def gen_config(self, kind, seed, param, m, begin, count, pitch=None):
+        """Pairs [begin, begin+count) of BASELINE config `kind` (1..4), byte-identical
+        to the device generator (csrc/datagen.cu). Returns (text, pattern) u8[count, pitch]."""
+        pitch = pitch or m
+        t = np.zeros((count, pitch), np.uint8)
+        p = np.zeros((count, pitch), np.uint8)
+        if count and self.lib.so_gen_config(kind, seed, param, m, begin, count, _ptr(t), _ptr(p),
+                                            pitch):
+            raise OracleError(-1)
+        return t, p
+
+    def gen_config_rows(self, kind, seed, param, m, rows):
+        """The generator's pairs at arbitrary indices `rows` -> (text, pattern) u8[k, m]."""
+        idx = np.ascontiguousarray(rows, dtype=np.uint64)
+        t = np.zeros((idx.size, m), np.uint8)
+        p = np.zeros((idx.size, m), np.uint8)
+        if idx.size and self.lib.so_gen_config_rows(kind, seed, param, m, _ptr(idx), idx.size,
+                                                    _ptr(t), _ptr(p), m):
+            raise OracleError(-1)
+        return t, p
+
+    def shouji_fast_batch(self, text, pattern, e, width=4, threads=None):
+        """Estimates u32[n] of validated records by the vectorisable restatement."""
+        text, pattern = _records(text, pattern)
+        n, m = text.shape
+        est = np.zeros(n, np.uint32)
+        st = self.lib.so_shouji_fast_batch(_ptr(text), _ptr(pattern), m, n, m, e, width,
+                                           threads or os.cpu_count() or 1, _ptr(est))
+        if st:
+            raise OracleError(st)
+        return est
+
+    def config_estimates(self, kind, seed, param, m, e, begin, count, width=4, threads=None):
+        """Estimates u32[count] of config pairs [begin, begin+count), generated on the fly."""
+        est = np.zeros(count, np.uint32)
+        st = self.lib.so_config_estimates(kind, seed, param, m, e, width, begin, count,
+                                          threads or os.cpu_count() or 1, _ptr(est))
+        if st:
+            raise OracleError(st)
+        return est
 
     def shouji_one(self, pattern: str, text: str, e: int, width: int = 4):
         """shouji_filter(seq(pattern), seq(text), e, width) -> (accept, estimate, bits str)."""

@@ -273,6 +273,12 @@ def transfer_bytes() -> tuple[int, int]:
     return int(h2d.value), int(d2h.value)
 
 
+def host_read_bandwidth(buf: np.ndarray, passes: int = 3) -> float:
+    """GB/s at which the host cores stream-read ``buf`` (pf_host_read_bandwidth)."""
+    buf = np.ascontiguousarray(buf)
+    return float(L.lib.pf_host_read_bandwidth(buf.ctypes.data_as(C.c_void_p), buf.nbytes, passes))
+
+
 def device_pitch(m: int) -> int:
     return int(L.lib.pf_device_pitch(m))
 

@@ -527,6 +527,13 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             if (!cu(cudaEventRecord(d.stage_ev[buf], d.stream), "stage record")) return;
         }
     }
+    if (pitch > m) {
+        // the last record's padding is read by the tile copies (never used): define it
+        const size_t tail = (n - 1) * pitch + m;
+        if (!cu(cudaMemsetAsync(d.d_text + tail, 'A', pitch - m, d.stream), "pad text") ||
+            !cu(cudaMemsetAsync(d.d_pattern + tail, 'A', pitch - m, d.stream), "pad pattern"))
+            return;
+    }
 
     // ---- kernels -----------------------------------------------------------
     if (!cu(cudaMemsetAsync(d.d_flag, 0, sizeof(uint32_t), d.stream), "memset flag")) return;
@@ -547,8 +554,10 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     const bool short_circuit = e >= m;
     const bool bad_width = !dist && !magnet && (width < 3 || width > 8);
     auto report_illegal = [&]() {
-        const unsigned long long init = ~0ull;
-        if (!cu(cudaMemcpy(d.d_key, &init, sizeof(init), cudaMemcpyHostToDevice), "key init")) return;
+        // the key is reset on the stream the locate kernel runs on (a legacy-stream
+        // cudaMemcpy is not ordered with a non-blocking stream)
+        if (!cu(cudaMemsetAsync(d.d_key, 0xFF, sizeof(unsigned long long), d.stream), "key init"))
+            return;
         if (!cu(sb::launch_locate(d.d_text, d.d_pattern, pitch, a.n, a.m, d.d_key, d.stream),
                 "locate"))
             return;
@@ -668,6 +677,10 @@ uint64_t pf_launch_count(void) { return sb::launch_count(); }
 void pf_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
     if (h2d) *h2d = g_h2d.load();
     if (d2h) *d2h = g_d2h.load();
+}
+
+double pf_host_read_bandwidth(const void* buf, size_t bytes, int passes) {
+    return sb::host_read_gbs(static_cast<const uint8_t*>(buf), bytes, passes);
 }
 
 size_t pf_nibble_pitch(uint32_t m) { return sb::nibble_pitch(static_cast<int>(std::max<uint32_t>(m, 1))); }
@@ -1128,8 +1141,7 @@ int pf_magnet_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
     PF_CUDA(cudaMemcpyAsync(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
     PF_CUDA(cudaStreamSynchronize(s));
     if (flag) {
-        const unsigned long long init = ~0ull;
-        PF_CUDA(cudaMemcpy(d.d_key, &init, sizeof(init), cudaMemcpyHostToDevice));
+        PF_CUDA(cudaMemsetAsync(d.d_key, 0xFF, sizeof(unsigned long long), s));  // key = ~0 on s
         PF_CUDA(sb::launch_locate(d_text, d_pattern, pitch, a.n, a.m, d.d_key, s));
         unsigned long long key = 0;
         PF_CUDA(cudaMemcpyAsync(&key, d.d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
@@ -1299,16 +1311,19 @@ int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
     a.planes_words = d.scratch_words;
     const bool short_circuit = e >= m;
     const bool bad_width = width < 3 || width > 8;
+    // The scratch (planes, and d_outplanes that bits_transpose reads) is held from
+    // the filter launch until after the transpose.
+    PF_CUDA(scratch_acquire(d, s));
     if (short_circuit || bad_width)
         PF_CUDA(sb::launch_validate(a, s));
     else
-        PF_CUDA(launch_any(d, a, s));
+        PF_CUDA(launch_any_unordered(d, a, s));
     uint32_t flag = 0;
     PF_CUDA(cudaMemcpyAsync(&flag, d.d_flag, sizeof(flag), cudaMemcpyDeviceToHost, s));
     PF_CUDA(cudaStreamSynchronize(s));
     if (flag) {
-        const unsigned long long init = ~0ull;
-        PF_CUDA(cudaMemcpy(d.d_key, &init, sizeof(init), cudaMemcpyHostToDevice));
+        PF_CUDA(scratch_release(d, s));
+        PF_CUDA(cudaMemsetAsync(d.d_key, 0xFF, sizeof(unsigned long long), s));  // key = ~0 on s
         PF_CUDA(sb::launch_locate(d_text, d_pattern, pitch, a.n, a.m, d.d_key, s));
         unsigned long long key = 0;
         PF_CUDA(cudaMemcpyAsync(&key, d.d_key, sizeof(key), cudaMemcpyDeviceToHost, s));
@@ -1317,6 +1332,7 @@ int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
         return PF_ERR_ILLEGAL_CHARACTER;
     }
     if (bad_width) {
+        PF_CUDA(scratch_release(d, s));
         set_err(err, PF_ERR_INVALID_PARAMETERS, "window width must be in [3, 8]");
         return PF_ERR_INVALID_PARAMETERS;
     }
@@ -1324,6 +1340,7 @@ int pf_shouji_filter_device(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* d
         PF_CUDA(sb::launch_accept_all(a.n, a.m, d_accept_bitmap, d_estimates, d_bits, s));
     else if (d_bits)
         PF_CUDA(sb::launch_bits_transpose(d.d_outplanes, a.n, a.m, d_bits, s));
+    PF_CUDA(scratch_release(d, s));
     return PF_OK;
 }
 
@@ -1373,8 +1390,16 @@ int pf_shouji_profile_stages(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* 
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceState& d = ctx->devs[0];
     PF_CUDA(cudaSetDevice(d.device));
-    cudaEvent_t ev[3];
-    for (auto& x : ev) PF_CUDA(cudaEventCreate(&x));
+    // events owned by a guard so that every early return (PF_CUDA) destroys them
+    struct Events {
+        cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+        ~Events() {
+            for (auto& x : e)
+                if (x) cudaEventDestroy(x);
+        }
+    } evs;
+    cudaEvent_t* ev = evs.e;
+    for (int i = 0; i < 3; ++i) PF_CUDA(cudaEventCreate(&ev[i]));
     sb::FilterArgs a{};
     a.text = d_text;
     a.pattern = d_pattern;
@@ -1398,7 +1423,6 @@ int pf_shouji_profile_stages(pf_ctx* ctx, const uint8_t* d_text, const uint8_t* 
         pk += t0;
         se += t1;
     }
-    for (auto& x : ev) cudaEventDestroy(x);
     *pack_ms = static_cast<float>(pk / reps);
     *search_ms = static_cast<float>(se / reps);
     return PF_OK;
@@ -1509,6 +1533,7 @@ int pf_generate_device(pf_ctx* ctx, int kind, uint64_t seed, uint32_t param, uin
                        uint8_t* d_pattern, size_t pitch, size_t n, uint32_t m, void* stream) {
     if (!ctx) return PF_ERR_NULL_ARGUMENT;
     pf_error* err = nullptr;
+    std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceState& d = ctx->devs[0];
     PF_CUDA(cudaSetDevice(d.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);

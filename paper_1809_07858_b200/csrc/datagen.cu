@@ -74,14 +74,18 @@ __device__ void apply_edit(char* s, int& size, int type, int lo, int hi, Rng& rn
     }
 }
 
-__device__ int poisson_inv(double mean, Rng& rng) {
+// Poisson(6) by inversion. exp(-6) is its correctly rounded double and every
+// step is rounded on its own (no FMA contraction), so the CPU mirror
+// (oracle/config_oracle.c, gen_poisson6) draws the same k bit for bit.
+__device__ int poisson_inv6(Rng& rng) {
     const double u = rng.uniform();
-    double p = exp(-mean), cdf = p;
+    double p = 0x1.44e51f113d4d6p-9;  // exp(-6)
+    double cdf = p;
     int k = 0;
     while (u > cdf && k < 200) {
         ++k;
-        p *= mean / k;
-        cdf += p;
+        p = __dmul_rn(p, __ddiv_rn(6.0, double(k)));
+        cdf = __dadd_rn(cdf, p);
     }
     return k;
 }
@@ -132,7 +136,7 @@ __global__ void generate_pairs_kernel(int kind, uint64_t seed, uint32_t param, u
             break;
         case 2:  // 30% unrelated, else k ~ Poisson(6)
             unrelated = rng.next() % 10 < 3;
-            k = poisson_inv(6.0, rng);
+            k = poisson_inv6(rng);
             break;
         case 3:  // k ~ U{0..2E}, half of the edits inside one 20-base burst
             k = int(rng.next() % uint64_t(2 * e + 1));

@@ -257,6 +257,14 @@ int pf_dataset_load_tsv(pf_ctx* ctx, const char* data, size_t len, const char* s
         const size_t tl = li.tab - li.begin, pl = li.end - li.tab - 1;
         if (!check_codec(data + li.begin, tl, line, err)) return PF_ERR_PARSE;
         if (!check_codec(data + li.tab + 1, pl, line, err)) return PF_ERR_PARSE;
+        if (tl == pl && tl >= (1u << 24) && (ls == 0 || tl == m)) {
+            // a well-formed line the reference would load: the records' length is
+            // beyond this implementation's limit (m < 2^24), not a length mismatch
+            set_parse(err, PF_ERR_INVALID_PARAMETERS, line,
+                      "line " + std::to_string(line) + ": sequence length " + std::to_string(tl) +
+                          " exceeds the supported maximum of " + std::to_string((1u << 24) - 1));
+            return PF_ERR_INVALID_PARAMETERS;
+        }
         if (tl != pl) {
             set_parse(err, PF_ERR_LENGTH_MISMATCH, line,
                       "length mismatch at line " + std::to_string(line) + ": " +

@@ -18,6 +18,7 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstdint>
@@ -417,6 +418,57 @@ void host_copy_parallel(void* dst, const void* src, size_t bytes) {
         body(0);
     else
         pool().run(tasks, body);
+}
+
+namespace {
+SB_AVX512 uint64_t stream_read_avx512(const uint8_t* p, size_t bytes) {
+    __m512i acc = _mm512_setzero_si512();
+    size_t i = 0;
+    for (; i + 256 <= bytes; i += 256) {
+        _mm_prefetch(reinterpret_cast<const char*>(p + i + 64 * 64), _MM_HINT_T0);
+        _mm_prefetch(reinterpret_cast<const char*>(p + i + 64 * 64 + 128), _MM_HINT_T0);
+        acc = _mm512_xor_si512(acc, _mm512_loadu_si512(p + i));
+        acc = _mm512_xor_si512(acc, _mm512_loadu_si512(p + i + 64));
+        acc = _mm512_xor_si512(acc, _mm512_loadu_si512(p + i + 128));
+        acc = _mm512_xor_si512(acc, _mm512_loadu_si512(p + i + 192));
+    }
+    uint64_t x = static_cast<uint64_t>(_mm512_reduce_add_epi64(acc));
+    for (; i < bytes; ++i) x += p[i];
+    return x;
+}
+}  // namespace
+
+double host_read_gbs(const uint8_t* buf, size_t bytes, int passes) {
+    // The host pack's own access pattern (AVX-512 loads, software prefetch 64 lines
+    // ahead) over a caller buffer, on the same worker pool: what the host cores can
+    // stream out of this memory, i.e. the ceiling of any path that reads it once.
+    if (!buf || bytes < (1u << 20) || passes < 1) return 0.0;
+    const bool simd = has_avx512();
+    const size_t tasks = 4ull * host_pack_threads();
+    std::vector<uint64_t> sink(tasks, 0);
+    auto body = [&](size_t t) {
+        const size_t lo = bytes * t / tasks / 64 * 64;
+        const size_t hi = t + 1 == tasks ? bytes : bytes * (t + 1) / tasks / 64 * 64;
+        if (simd) {
+            sink[t] += stream_read_avx512(buf + lo, hi - lo);
+        } else {
+            uint64_t x = 0;
+            for (size_t i = lo; i + 8 <= hi; i += 8) {
+                uint64_t v;
+                std::memcpy(&v, buf + i, 8);
+                x ^= v;
+            }
+            sink[t] += x;
+        }
+    };
+    pool().run(tasks, body);  // warm (page tables, worker wake-up)
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < passes; ++r) pool().run(tasks, body);
+    const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    volatile uint64_t keep = 0;
+    for (auto v : sink) keep = keep + v;
+    (void)keep;
+    return s > 0 ? double(bytes) * passes / s / 1e9 : 0.0;
 }
 
 void host_pack_dibits_parallel(const uint8_t* text, const uint8_t* pattern, size_t stride,

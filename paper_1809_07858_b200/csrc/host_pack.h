@@ -54,6 +54,10 @@ void host_validate_parallel(const uint8_t* text, const uint8_t* pattern, size_t 
 // memcpy on the same worker pool (pageable -> pinned staging copies).
 void host_copy_parallel(void* dst, const void* src, size_t bytes);
 
+// Stream-read bandwidth of the host cores over buf (GB/s, `passes` timed passes
+// after one warm pass), with the host pack's access pattern on its worker pool.
+double host_read_gbs(const uint8_t* buf, size_t bytes, int passes);
+
 // True when the AVX-512 (BW/VBMI) path is used on this host.
 bool host_pack_uses_simd();
 

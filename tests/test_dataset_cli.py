@@ -123,3 +123,17 @@ def test_load_tsv_from_a_fifo(oracle, tmp_path):
     st, _, rec = _load_file(fifo)
     w.join()
     assert st == 0 and (rec[0] == t).all() and (rec[1] == p).all()
+
+
+def test_load_tsv_line_beyond_length_limit(tmp_path):
+    # A well-formed first line the reference would load, with records longer than this
+    # implementation's m < 2^24 limit: reported as an invalid parameter with its own
+    # message, not as a length mismatch of the line against itself.
+    from paper_1809_07858_b200 import _lib as L
+    k = 1 << 24
+    f = tmp_path / "long.tsv"
+    f.write_bytes(b"A" * k + b"\t" + b"C" * k + b"\n")
+    st, err, _ = _load_file(f)
+    assert st == L.PF_ERR_INVALID_PARAMETERS and err.line == 1
+    assert b"exceeds the supported maximum" in bytes(err.message)
+    assert b"length mismatch" not in bytes(err.message)
