@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -24,6 +25,7 @@
 #include "host_pack.h"
 #include "kernels.cuh"
 #include "pack.cuh"
+#include "split.h"
 
 namespace {
 
@@ -80,6 +82,9 @@ struct DeviceState {
     // last use of the plane scratch (d_scratch) on any stream:
     // device calls on caller streams and host batches on `stream` share them
     cudaEvent_t scratch_ev = nullptr;
+    // SM-partitioned pack | search pipeline (split.cpp), created on first use
+    sb::SplitPipe* split = nullptr;
+    int split_sms = -1;  // pack SMs the pipe was built for (-1: none tried)
 };
 
 }  // namespace
@@ -148,7 +153,43 @@ cudaError_t launch_any(DeviceState& d, sb::FilterArgs a, cudaStream_t s) {
     return st;
 }
 
+// Pack | search on disjoint SM partitions (split.cpp) for device-resident ASCII
+// records with the width-4 search: PF_SPLIT = pack SMs (0 = off), PF_SPLIT_CHUNK =
+// pairs per chunk. Read per call so that A/B sweeps can change them in-process.
+int split_pack_sms_setting() {
+    const char* e = std::getenv("PF_SPLIT");
+    return e ? std::atoi(e) : 0;
+}
+long long split_chunk_setting() {
+    const char* e = std::getenv("PF_SPLIT_CHUNK");
+    const long long v = e ? std::atoll(e) : 0;
+    return v > 0 ? v : (3ll << 20);
+}
+
+bool split_applies(const sb::FilterArgs& a) {
+    return !a.nibbles && !a.dibits && !a.packed_text && a.stage_event == nullptr &&
+           a.outplanes == nullptr && sb::use_fused(a.width, a.e, a.m) &&
+           a.n >= 2 * split_chunk_setting();
+}
+
+sb::SplitPipe* split_pipe(DeviceState& d) {
+    const int want = split_pack_sms_setting();
+    if (want <= 0) return nullptr;
+    if (d.split_sms != want) {
+        sb::split_destroy(d.split);
+        std::string why;
+        d.split = sb::split_create(d.device, want, &why);
+        d.split_sms = want;
+        if (!d.split && std::getenv("PF_SPLIT_VERBOSE"))
+            std::fprintf(stderr, "pf: SM split unavailable (%s); serial pack + search\n", why.c_str());
+    }
+    return d.split;
+}
+
 cudaError_t launch_any_unordered(DeviceState& d, sb::FilterArgs a, cudaStream_t s) {
+    if (split_applies(a)) {
+        if (sb::SplitPipe* sp = split_pipe(d)) return sb::split_launch(sp, a, s, split_chunk_setting());
+    }
     const cudaError_t st = grow(d.d_scratch, d.scratch_words, sb::planes_scratch_words(a.n, a.m));
     if (st != cudaSuccess) return st;
     a.planes = d.d_scratch;
@@ -878,6 +919,8 @@ void pf_ctx_destroy(pf_ctx* ctx) {
         cudaFree(d.d_outplanes);
         cudaFree(d.d_scratch);
         if (d.scratch_ev) cudaEventDestroy(d.scratch_ev);
+        sb::split_destroy(d.split);
+        d.split = nullptr;
         cudaFree(d.d_flag);
         cudaFree(d.d_key);
         cudaFree(d.d_stage);

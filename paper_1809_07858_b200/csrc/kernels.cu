@@ -310,15 +310,44 @@ static bool nflags_enabled() {
 
 static bool search_reads_nflags(const FilterArgs& a) { return use_fused(a.width, a.e, a.m); }
 
-cudaError_t launch_filter(const FilterArgs& args, cudaStream_t s) {
-    if (args.n <= 0) return cudaSuccess;
-    if (args.planes == nullptr || args.planes_words < plane_words(args.n, args.m))
-        return cudaErrorInvalidValue;
+// The N-presence flag region both stages agree on (or null).
+static FilterArgs resolve_nflags(const FilterArgs& args) {
     FilterArgs a = args;
     a.nflags = nullptr;
     if (nflags_enabled() && args.planes_words >= planes_scratch_words(a.n, a.m) &&
         search_reads_nflags(a) && pack_writes_nflags(a))
         a.nflags = a.planes + plane_words(a.n, a.m);
+    return a;
+}
+
+static cudaError_t launch_pack_of(const FilterArgs& a, cudaStream_t s) {
+    return a.packed_text ? launch_pack_planes(a.packed_text, a.packed_pattern, a.n, a.m, a.planes, s)
+           : a.dibits    ? launch_pack_dibits(a.text, a.pattern, a.ntext, a.npattern, a.n, a.m,
+                                              a.planes, s, a.nflags)
+           : a.nibbles   ? launch_pack_nibbles(a.text, a.pattern, a.n, a.m, a.planes, s, a.nflags)
+                         : launch_pack(a.text, a.pattern, a.pitch, a.n, a.m, a.planes, a.err_flag, s,
+                                       a.nflags);
+}
+
+static cudaError_t launch_search_of(const FilterArgs& a, cudaStream_t s) {
+    if (use_fused(a.width, a.e, a.m)) return kSearchTable[a.e](a, s);
+    if (wsearch_enabled() && wsearch_applies(a)) return launch_wsearch(a, s);
+    return a.m <= 255 ? launch_generic<8>(a, s) : launch_generic<24>(a, s);
+}
+
+cudaError_t launch_filter_stage(const FilterArgs& args, cudaStream_t s, int stage) {
+    if (args.n <= 0) return cudaSuccess;
+    if (args.planes == nullptr || args.planes_words < plane_words(args.n, args.m))
+        return cudaErrorInvalidValue;
+    const FilterArgs a = resolve_nflags(args);
+    return stage == 1 ? launch_pack_of(a, s) : launch_search_of(a, s);
+}
+
+cudaError_t launch_filter(const FilterArgs& args, cudaStream_t s) {
+    if (args.n <= 0) return cudaSuccess;
+    if (args.planes == nullptr || args.planes_words < plane_words(args.n, args.m))
+        return cudaErrorInvalidValue;
+    FilterArgs a = resolve_nflags(args);
     cudaError_t st =
         a.packed_text ? launch_pack_planes(a.packed_text, a.packed_pattern, a.n, a.m, a.planes, s)
         : a.dibits    ? launch_pack_dibits(a.text, a.pattern, a.ntext, a.npattern, a.n, a.m,

@@ -83,6 +83,9 @@ cudaError_t launch_pack_planes(const uint64_t* text, const uint64_t* pattern, lo
                                uint32_t* planes, cudaStream_t s);
 // Launch the filter (pack + width-4 search, or pack + generic). Returns a cudaError_t.
 cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s);
+// One stage of launch_filter on its own stream: 1 = pack into a.planes, 2 = search
+// from them (same FilterArgs for both; the caller orders stage 2 after stage 1).
+cudaError_t launch_filter_stage(const FilterArgs& a, cudaStream_t s, int stage);
 // Validation only (for e >= m or an invalid width): sets *err_flag on any illegal byte.
 cudaError_t launch_validate(const FilterArgs& a, cudaStream_t s);
 // First illegal byte: key = ((pair*2+field) << 24) | pos into *d_key (pre-set to ~0).

@@ -13,7 +13,10 @@ oracle/config_oracle.c), and this script records
 * ``estimate_sha256`` — sha256 of the estimates as u32 little endian, one per pair;
 * ``accepted`` and ``estimate_hist`` (readable summaries of the same data);
 * ``data_prefix_sha256`` — sha256 of the set's first 4096 pairs' bytes (the
-  generator mirror's output; text rows then pattern rows).
+  generator mirror's output; text rows then pattern rows);
+* ``estimate_prefix_sha256`` — sha256 of the first 65536 pairs' estimates, which
+  the CPU suite recomputes with the reference library itself
+  (tests/test_oracle_configs.py).
 
 tests/test_gpu_fullsize_digests.py regenerates each set on the device and
 compares the GPU's own bitmap and estimates against these digests.
@@ -122,10 +125,20 @@ def run_reference(s, o, ref, threads, limit=None):
     return n, d.result()
 
 
-def data_prefix(s, o, k=4096):
+PREFIX_PAIRS = 4096
+ESTIMATE_PREFIX_PAIRS = 1 << 16
+
+
+def data_prefix(s, o, k=PREFIX_PAIRS):
     """sha256 of the set's first k pairs (text rows then pattern rows, m bytes each)."""
     t, p = o.gen_config(s["config"], s["seed"], s["E"], s["m"], 0, k)
     return hashlib.sha256(t.tobytes() + p.tobytes()).hexdigest()
+
+
+def estimate_prefix(s, o, k=ESTIMATE_PREFIX_PAIRS, threads=None):
+    """sha256 of the estimates (u32 LE) of the set's first k pairs."""
+    est = o.config_estimates(s["config"], s["seed"], s["E"], s["m"], s["E"], 0, k, threads=threads)
+    return hashlib.sha256(est.astype("<u4").tobytes()).hexdigest()
 
 
 def key(s):
@@ -152,6 +165,7 @@ def main():
         rec = dict(have.get(key(s), s))
         t0 = time.time()
         rec["data_prefix_sha256"] = data_prefix(s, o)
+        rec["estimate_prefix_sha256"] = estimate_prefix(s, o, threads=args.threads)
         if args.data_prefix_only:
             pass
         elif args.ref_prefix or args.ref_full:

@@ -88,18 +88,29 @@ def test_generator_config_properties(oracle):
 
 
 def test_digest_file_pins_the_generator_prefix(oracle):
-    """The committed digests were computed on the mirror's bytes: recompute the first
-    chunk's estimates of one set per config and compare with a fresh digest of the
-    same prefix taken by the script's own code."""
+    """Every committed set still matches the mirror's bytes (data_prefix_sha256)."""
     doc = json.load(open(mfd.OUT))
-    by = {(s["config"], s["E"]): s for s in doc["sets"]}
-    for config, e in [(1, 5), (2, 7), (3, 25), (4, 25)]:
-        s = by[(config, e)]
-        assert s["seed"] == mfd.seed_of(config, e)
-        if "data_prefix_sha256" in s:
-            t, p = oracle.gen_config(config, s["seed"], e, s["m"], 0, 4096)
-            h = hashlib.sha256(t.tobytes() + p.tobytes()).hexdigest()
-            assert h == s["data_prefix_sha256"], (config, e)
+    assert len(doc["sets"]) == len(mfd.all_sets())
+    for s in doc["sets"]:
+        assert s["seed"] == mfd.seed_of(s["config"], s["E"])
+        t, p = oracle.gen_config(s["config"], s["seed"], s["E"], s["m"], 0, mfd.PREFIX_PAIRS)
+        h = hashlib.sha256(t.tobytes() + p.tobytes()).hexdigest()
+        assert h == s["data_prefix_sha256"], (s["config"], s["E"])
+
+
+@pytest.mark.parametrize("config", [1, 2, 3, 4])
+def test_reference_library_reproduces_the_estimate_prefixes(oracle, reference, config):
+    """The unmodified reference library recomputes the first 65536 pairs of every
+    committed set of this config and hashes to the recorded estimate_prefix_sha256."""
+    doc = json.load(open(mfd.OUT))
+    sets = [s for s in doc["sets"] if s["config"] == config]
+    if config == 3:  # the 26-threshold sweep: every fifth E on CPU (all of them on the GPU)
+        sets = [s for s in sets if s["E"] % 5 == 0 or s["E"] == 25]
+    for s in sets:
+        t, p = oracle.gen_config(config, s["seed"], s["E"], s["m"], 0, mfd.ESTIMATE_PREFIX_PAIRS)
+        _, est, _ = reference.shouji_batch(t, p, s["E"])
+        h = hashlib.sha256(est.astype("<u4").tobytes()).hexdigest()
+        assert h == s["estimate_prefix_sha256"], (config, s["E"])
 
 
 def test_bitmap_layout_matches_the_c_abi(oracle):
