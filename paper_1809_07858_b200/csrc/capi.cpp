@@ -82,6 +82,15 @@ struct DeviceState {
     // last use of the plane scratch (d_scratch) on any stream:
     // device calls on caller streams and host batches on `stream` share them
     cudaEvent_t scratch_ev = nullptr;
+    // latency path (small.cu): mapped pinned staging, host pointer + device alias
+    uint8_t* h_small_in = nullptr;
+    uint8_t* d_small_in = nullptr;
+    size_t small_in_bytes = 0;
+    uint8_t* h_small_out = nullptr;
+    uint8_t* d_small_out = nullptr;
+    size_t small_out_bytes = 0;
+    unsigned* d_small_counter = nullptr;  // CTA completion count (device)
+    unsigned small_seq = 0;
     // SM-partitioned pack | search pipeline (split.cpp), created on first use
     sb::SplitPipe* split = nullptr;
     int split_sms = -1;  // pack SMs the pipe was built for (-1: none tried)
@@ -921,6 +930,9 @@ void pf_ctx_destroy(pf_ctx* ctx) {
         if (d.scratch_ev) cudaEventDestroy(d.scratch_ev);
         sb::split_destroy(d.split);
         d.split = nullptr;
+        if (d.h_small_in) cudaFreeHost(d.h_small_in);
+        if (d.h_small_out) cudaFreeHost(d.h_small_out);
+        cudaFree(d.d_small_counter);
         cudaFree(d.d_flag);
         cudaFree(d.d_key);
         cudaFree(d.d_stage);
@@ -1071,6 +1083,111 @@ void run_packed_shard(DeviceState& d, const uint64_t* text, const uint64_t* patt
     cu(cudaStreamSynchronize(d.stream), "sync");
 }
 
+// ---- latency path: small batches ------------------------------------------------
+// A per-pair caller (shouji_filter's signature, or the drop-in's coalesced
+// handful of pairs) pays one launch of the latency kernel (small.cu) and one
+// synchronisation: inputs are copied into mapped pinned staging that the kernel
+// reads in place, and the kernel writes the bitmap, estimates and tally words
+// straight back into mapped memory. PF_SMALL=0 turns it off (A/B runs).
+bool small_applies(size_t n, uint32_t m) {
+    const char* env = std::getenv("PF_SMALL");  // read per call: tests A/B both paths
+    const bool on = !(env && env[0] == '0');
+    return on && n <= static_cast<size_t>(sb::kSmallMaxN) && m <= static_cast<uint32_t>(sb::kSmallMaxM);
+}
+
+cudaError_t grow_mapped(uint8_t*& h, uint8_t*& dptr, size_t& have, size_t need) {
+    if (need <= have && h) return cudaSuccess;
+    if (h) cudaFreeHost(h);
+    h = dptr = nullptr;
+    have = 0;
+    cudaError_t st = cudaHostAlloc(reinterpret_cast<void**>(&h), need,
+                                   cudaHostAllocMapped | cudaHostAllocPortable);
+    if (st != cudaSuccess) return st;
+    st = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), h, 0);
+    if (st != cudaSuccess) return st;
+    have = need;
+    return cudaSuccess;
+}
+
+int run_small(DeviceState& d, const uint8_t* text, const uint8_t* pattern, size_t stride,
+              const uint64_t* tplanes, const uint64_t* pplanes, size_t n, uint32_t m, uint32_t e,
+              uint32_t width, uint32_t* accept_bitmap, uint32_t* estimates, uint64_t* bits,
+              pf_error* err) {
+    PF_CUDA(cudaSetDevice(d.device));
+    const size_t W = (m + 63) / 64;
+    const size_t acc_words = (n + 31) / 32;
+    const size_t in_bytes = text ? 2 * n * m : 2 * n * 3 * W * sizeof(uint64_t);
+    // out: key (8 B), done flag (8 B), bits (n*W u64), estimates, accept bytes
+    const size_t off_done = 8, off_bits = 16, off_est = off_bits + n * W * 8, off_acc = off_est + n * 4;
+    const size_t out_bytes = off_acc + n;
+    PF_CUDA(grow_mapped(d.h_small_in, d.d_small_in, d.small_in_bytes, std::max<size_t>(in_bytes, 4096)));
+    PF_CUDA(grow_mapped(d.h_small_out, d.d_small_out, d.small_out_bytes, std::max<size_t>(out_bytes, 4096)));
+    sb::SmallArgs a{};
+    if (text) {
+        for (size_t i = 0; i < n; ++i) {
+            std::memcpy(d.h_small_in + i * m, text + i * stride, m);
+            std::memcpy(d.h_small_in + (n + i) * m, pattern + i * stride, m);
+        }
+        a.text = d.d_small_in;
+        a.pattern = d.d_small_in + n * m;
+        a.stride = m;
+    } else {
+        const size_t pw = 3 * W;
+        std::memcpy(d.h_small_in, tplanes, n * pw * 8);
+        std::memcpy(d.h_small_in + n * pw * 8, pplanes, n * pw * 8);
+        a.tplanes = reinterpret_cast<const uint64_t*>(d.d_small_in);
+        a.pplanes = reinterpret_cast<const uint64_t*>(d.d_small_in + n * pw * 8);
+    }
+    auto* key = reinterpret_cast<volatile unsigned long long*>(d.h_small_out);
+    *key = ~0ull;
+    a.n = static_cast<int>(n);
+    a.m = static_cast<int>(m);
+    a.e = e;
+    a.w = static_cast<int>(width);
+    a.accept = d.d_small_out + off_acc;
+    a.est = reinterpret_cast<uint32_t*>(d.d_small_out + off_est);
+    a.bits = bits ? reinterpret_cast<uint64_t*>(d.d_small_out + off_bits) : nullptr;
+    a.bad_key = text ? reinterpret_cast<unsigned long long*>(d.d_small_out) : nullptr;
+    if (!d.d_small_counter) {
+        PF_CUDA(cudaMalloc(&d.d_small_counter, sizeof(unsigned)));
+        PF_CUDA(cudaMemset(d.d_small_counter, 0, sizeof(unsigned)));
+    }
+    a.counter = d.d_small_counter;
+    a.done = reinterpret_cast<volatile unsigned*>(d.d_small_out + off_done);
+    a.seq = ++d.small_seq;
+    auto* done = reinterpret_cast<volatile unsigned*>(d.h_small_out + off_done);
+    PF_CUDA(sb::launch_small(a, d.stream));
+    // completion: the kernel's last CTA publishes seq into mapped memory after a
+    // system fence; polling it costs less than a stream synchronisation. The
+    // stream is queried now and then so that a failed launch cannot spin forever.
+    for (unsigned spin = 1; *done != a.seq; ++spin) {
+        if ((spin & 255) == 0) {
+            const cudaError_t q = cudaStreamQuery(d.stream);
+            if (q == cudaErrorNotReady) continue;
+            PF_CUDA(q);
+            if (*done != a.seq) {  // stream idle but no flag: should not happen
+                set_err(err, PF_ERR_CUDA, "latency kernel finished without its completion flag");
+                return PF_ERR_CUDA;
+            }
+        }
+    }
+    if (text && *key != ~0ull) {
+        decode_illegal(*key, 0, text, pattern, stride, true, err);
+        return PF_ERR_ILLEGAL_CHARACTER;
+    }
+    if (width < 3 || width > 8) {  // window_zero_table ctor (shouji.cpp:9-15)
+        set_err(err, PF_ERR_INVALID_PARAMETERS, "window width must be in [3, 8]");
+        return PF_ERR_INVALID_PARAMETERS;
+    }
+    std::memset(accept_bitmap, 0, acc_words * 4);
+    const uint8_t* acc8 = d.h_small_out + off_acc;
+    for (size_t i = 0; i < n; ++i)
+        if (acc8[i]) accept_bitmap[i / 32] |= 1u << (i % 32);
+    if (estimates) std::memcpy(estimates, d.h_small_out + off_est, n * 4);
+    if (bits) std::memcpy(bits, d.h_small_out + off_bits, n * W * 8);
+    return PF_OK;
+}
+
 int run_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t stride, size_t n,
               uint32_t m, uint32_t e, uint32_t width, uint32_t* accept_bitmap, uint32_t* estimates,
               uint64_t* bits, int32_t* dist, pf_error* err, bool magnet = false) {
@@ -1091,6 +1208,9 @@ int run_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t s
         return PF_ERR_INVALID_PARAMETERS;
     }
     std::lock_guard<std::mutex> lock(ctx->mu);
+    if (!dist && !magnet && small_applies(n, m))
+        return run_small(ctx->devs[0], text, pattern, stride, nullptr, nullptr, n, m, e, width,
+                         accept_bitmap, estimates, bits, err);
     const size_t nd = ctx->devs.size();
     // contiguous 32-aligned shards (parallel_for_pairs' n*t/T split, evaluate.cpp:36-37)
     const size_t groups = (n + 31) / 32;
@@ -1223,6 +1343,9 @@ int pf_shouji_filter_packed_batch(pf_ctx* ctx, const uint64_t* text_planes,
         return PF_ERR_INVALID_PARAMETERS;
     }
     std::lock_guard<std::mutex> lock(ctx->mu);
+    if (small_applies(n, m))
+        return run_small(ctx->devs[0], nullptr, nullptr, 0, text_planes, pattern_planes, n, m, e,
+                         width, accept_bitmap, estimates, bits, err);
     const size_t nd = ctx->devs.size();
     const size_t groups = (n + 31) / 32;
     std::vector<size_t> bounds(nd + 1);

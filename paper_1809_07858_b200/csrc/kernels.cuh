@@ -114,6 +114,34 @@ cudaError_t launch_magnet_dibits(const uint8_t* text, const uint8_t* pattern, co
                                  const uint8_t* npattern, long long n, int m, int e,
                                  uint32_t* accept, uint32_t* estimates, uint64_t* bits,
                                  cudaStream_t s);
+// Latency form for small batches (small.cu): one CTA per pair, windows over the
+// threads. ASCII records (text/pattern/stride; validated, first illegal byte into
+// *bad_key as launch_locate encodes it) or packed_sequence planes (tplanes/pplanes,
+// [n][3][ceil(m/64)] u64). accept: one byte per pair (0/1); est and bits may be
+// null. Any pointer may be a mapped pinned host alias.
+constexpr int kSmallMaxM = 2048;
+constexpr long long kSmallMaxN = 64;
+struct SmallArgs {
+    const uint8_t* text;
+    const uint8_t* pattern;
+    size_t stride;
+    const uint64_t* tplanes;
+    const uint64_t* pplanes;
+    int n;
+    int m;
+    uint32_t e;
+    int w;
+    uint8_t* accept;
+    uint32_t* est;
+    uint64_t* bits;
+    unsigned long long* bad_key;
+    unsigned* counter;         // device word, 0 between launches (null: no done flag)
+    volatile unsigned* done;   // receives seq when every CTA has finished
+    unsigned seq;
+};
+size_t small_smem_bytes(int m, uint32_t e);
+cudaError_t launch_small(const SmallArgs& a, cudaStream_t s);
+
 // e >= m short-circuit outputs.
 cudaError_t launch_accept_all(long long n, int m, uint32_t* accept, uint32_t* estimates,
                               uint64_t* bits, cudaStream_t s);

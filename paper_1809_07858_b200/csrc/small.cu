@@ -1,0 +1,208 @@
+// Latency form of the Shouji filter for small batches: a per-pair caller of
+// shouji_filter (proj/src/shouji.cpp:41-58), or the few pairs the drop-in's
+// coalescer gathers from concurrent callers. The throughput kernels slice 32
+// pairs into every register word and sweep a pair's windows serially inside
+// one thread (~50 µs for one group); here one CTA owns one pair and spreads
+// its m windows over the threads instead:
+//   * codes: the pair's bases from ASCII records (validated like
+//     packed_sequence::from_string, packed_sequence.cpp:19-29; the first
+//     illegal byte in pair order, text before pattern, is reported through the
+//     same key as the locate kernel) or from packed_sequence planes;
+//   * select_window (shouji.cpp:17-31): thread j scans d = -e..+e in reference
+//     order over its own window with the reference's two-clause rule — more
+//     zeros, or equal zeros with the incumbent's bit 0 set and the candidate's
+//     clear; a mismatch cell is "codes differ", with N coded differently in
+//     pattern and text and out-of-range columns coded apart from every base,
+//     exactly neighborhood.cpp:67-76 and extract(pos, w, pad = 1);
+//   * commit_window (shouji.cpp:33-39): the serial strict-improvement overwrite
+//     over j, one thread, in shared memory; then the tally popcount and
+//     accept = ones <= e (:56-57), e >= m accepting with estimate 0 (:48-49).
+// Inputs and outputs may live in mapped pinned host memory (the host entry
+// points pass device aliases of their staging buffers), so a call is one
+// launch and one synchronisation; outputs are plain stores (one accept byte per
+// pair, no atomics to host memory).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace sb {
+
+namespace {
+
+__device__ __forceinline__ uint8_t code_ascii(uint8_t c, uint8_t ncode, bool* bad) {
+    switch (c) {
+        case 'A': return 0;
+        case 'C': return 1;
+        case 'G': return 2;
+        case 'T': return 3;
+        case 'N': return ncode;
+        default: *bad = true; return ncode;
+    }
+}
+
+// The last CTA to finish publishes a.seq into *a.done (mapped host memory)
+// after a system-scope fence, so the host can poll for completion instead of
+// paying a stream synchronisation.
+__device__ void finish(const SmallArgs& a) {
+    if (a.done == nullptr) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(a.counter, 1u) == static_cast<unsigned>(a.n) - 1u) {
+            *a.counter = 0u;
+            __threadfence_system();
+            *a.done = a.seq;
+        }
+    }
+}
+
+__global__ void shouji_small_kernel(SmallArgs a) {
+    extern __shared__ uint8_t sm[];
+    const int m = a.m, w = a.w, pair = blockIdx.x;
+    const bool select = a.e < static_cast<uint32_t>(m) && w >= 3 && w <= 8;
+    const int e = select ? static_cast<int>(a.e) : 0;
+    uint8_t* pc = sm;                  // pattern codes at [e, e+m); 6 outside
+    uint8_t* tc = pc + m + 2 * e + 16;  // text codes; 7 past m
+    uint8_t* bs = tc + m + 16;          // best slice per window
+    uint8_t* bz = bs + m + 16;          // its zero count
+    uint8_t* bv = bz + m + 16;          // tally bits; 1 past m
+    __shared__ uint32_t ones_total;
+    __shared__ int bad_here;
+    if (threadIdx.x == 0) {
+        ones_total = 0;
+        bad_here = 0;
+    }
+
+    for (int i = threadIdx.x; i < m + 2 * e + 16; i += blockDim.x) pc[i] = 6;
+    for (int i = threadIdx.x; i < m + 16; i += blockDim.x) {
+        tc[i] = 7;
+        bv[i] = 1;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        uint8_t p, t;
+        if (a.text != nullptr) {
+            bool bt = false, bp = false;
+            t = code_ascii(a.text[static_cast<size_t>(pair) * a.stride + i], 5, &bt);
+            p = code_ascii(a.pattern[static_cast<size_t>(pair) * a.stride + i], 4, &bp);
+            // locate key ((pair*2 + field) << 24) | pos, as launch_locate writes it
+            // (global atomics only on the error path: a.bad_key may be host memory)
+            if (bt) {
+                atomicMin(a.bad_key, ((static_cast<unsigned long long>(pair) * 2) << 24) | i);
+                bad_here = 1;
+            }
+            if (bp) {
+                atomicMin(a.bad_key, ((static_cast<unsigned long long>(pair) * 2 + 1) << 24) | i);
+                bad_here = 1;
+            }
+        } else {
+            const int W = (m + 63) / 64;
+            const uint64_t* tp = a.tplanes + static_cast<size_t>(pair) * 3 * W;
+            const uint64_t* pp = a.pplanes + static_cast<size_t>(pair) * 3 * W;
+            const int wd = i >> 6, b = i & 63;
+            t = ((tp[2 * W + wd] >> b) & 1u) ? 5
+                                              : static_cast<uint8_t>(((tp[wd] >> b) & 1u) |
+                                                                     (((tp[W + wd] >> b) & 1u) << 1));
+            p = ((pp[2 * W + wd] >> b) & 1u) ? 4
+                                              : static_cast<uint8_t>(((pp[wd] >> b) & 1u) |
+                                                                     (((pp[W + wd] >> b) & 1u) << 1));
+        }
+        tc[i] = t;
+        pc[e + i] = p;
+    }
+    __syncthreads();
+    if (bad_here || (!select && (w < 3 || w > 8))) {
+        finish(a);  // the host reports the illegal byte, or the width; no results
+        return;
+    }
+    if (!select) {
+        // e >= m: accept, estimate 0, all-zero tally (shouji.cpp:48-49)
+        if (threadIdx.x == 0) {
+            a.accept[pair] = 1;
+            if (a.est) a.est[pair] = 0;
+        }
+        if (a.bits)
+            for (int k = threadIdx.x; k < (m + 63) / 64; k += blockDim.x)
+                a.bits[static_cast<size_t>(pair) * ((m + 63) / 64) + k] = 0;
+        finish(a);
+        return;
+    }
+    // select_window for every window j, diagonals in reference order
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        uint8_t best_s = 0, best_z = 0;
+        for (int d = -e; d <= e; ++d) {
+            const uint8_t* prow = pc + e + d + j;
+            unsigned s = 0, ones = 0;
+            for (int k = 0; k < w; ++k) {
+                const unsigned x = prow[k] != tc[j + k];
+                s |= x << k;
+                ones += x;
+            }
+            const uint8_t z = static_cast<uint8_t>(w - ones);
+            if (d == -e || z > best_z || (z == best_z && (best_s & 1u) && !(s & 1u))) {
+                best_s = static_cast<uint8_t>(s);
+                best_z = z;
+            }
+        }
+        bs[j] = best_s;
+        bz[j] = best_z;
+    }
+    __syncthreads();
+    // commit_window, serially over j, as a (w-1)-bit state machine in registers
+    // (SURVEY App. B2 for general w): when window j is examined, bv[j+w-1] is
+    // still 1 (no earlier window reaches it), so the incumbent's zeros are those
+    // of S = bv[j .. j+w-2] (bit i = column j+i; columns >= m read as 1, the
+    // pad of extract(pos, w, pad = 1)). Strict improvement: commit iff
+    // zeros(best) > (w-1) - popcount(S); the committed slice's overhang is
+    // dropped (deposit, bitvector.hpp:97-100), i.e. read back as 1.
+    if (threadIdx.x == 0) {
+        const unsigned full = (1u << (w - 1)) - 1u;
+        unsigned S = full;  // bv starts all ones (shouji.cpp:52)
+        for (int j = 0; j < m; ++j) {
+            const unsigned z = bz[j], sl = bs[j];
+            const bool commit = z + static_cast<unsigned>(__popc(S)) > static_cast<unsigned>(w - 1);
+            // columns j+1 .. j+w-1 after the step; those >= m read as 1
+            const int past = j + w - m;  // columns j+w-1-past+1 .. j+w-1 are past the end
+            const unsigned pad = past > 0 ? (full << (w - 1 - (past < w - 1 ? past : w - 1))) & full
+                                          : 0u;
+            bv[j] = static_cast<uint8_t>(commit ? (sl & 1u) : (S & 1u));
+            S = (commit ? (sl >> 1) : ((S >> 1) | (1u << (w - 2)))) | pad;
+        }
+    }
+    __syncthreads();
+    // tally bits (bitvector words) and the popcount
+    const int W = (m + 63) / 64;
+    for (int k = threadIdx.x; k < W; k += blockDim.x) {
+        uint64_t word = 0;
+        for (int b = 0; b < 64 && 64 * k + b < m; ++b)
+            word |= static_cast<uint64_t>(bv[64 * k + b]) << b;
+        if (a.bits) a.bits[static_cast<size_t>(pair) * W + k] = word;
+        atomicAdd(&ones_total, static_cast<uint32_t>(__popcll(word)));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (a.est) a.est[pair] = ones_total;
+        a.accept[pair] = ones_total <= a.e ? 1 : 0;
+    }
+    finish(a);
+}
+
+}  // namespace
+
+size_t small_smem_bytes(int m, uint32_t e) {
+    const size_t ee = e < static_cast<uint32_t>(m) ? e : 0;
+    return 5 * static_cast<size_t>(m) + 2 * ee + 80;
+}
+
+cudaError_t launch_small(const SmallArgs& a, cudaStream_t s) {
+    if (a.n <= 0) return cudaSuccess;
+    if (a.m < 1 || a.m > kSmallMaxM) return cudaErrorInvalidValue;
+    const int threads = a.m <= 128 ? 128 : (a.m <= 256 ? 256 : 512);
+    shouji_small_kernel<<<a.n, threads, small_smem_bytes(a.m, a.e), s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace sb

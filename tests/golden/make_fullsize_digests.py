@@ -149,6 +149,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--threads", type=int, default=os.cpu_count())
     ap.add_argument("--only", default="", help="comma-separated config numbers")
+    ap.add_argument("--e-list", default="", help="comma-separated thresholds (default: all)")
     ap.add_argument("--ref-prefix", type=int, default=0)
     ap.add_argument("--ref-full", action="store_true")
     ap.add_argument("--data-prefix-only", action="store_true",
@@ -161,6 +162,8 @@ def main():
     have = {key(s): s for s in doc.get("sets", [])}
     for s in all_sets():
         if only and s["config"] not in only:
+            continue
+        if args.e_list and s["E"] not in {int(x) for x in args.e_list.split(",")}:
             continue
         rec = dict(have.get(key(s), s))
         t0 = time.time()

@@ -51,3 +51,19 @@ def dev():
 print("device async + sync", bench(dev), "us")
 print("python per-pair API", bench(lambda: pf.shouji_filter(pf.seq("GGTGAGAGTTGT" * 8),
                                                             pf.seq("GGTGCAGAGCTC" * 8), 5)), "us")
+
+# per-pair entry point (pf_shouji_filter_one -> latency kernel, csrc/small.cu), m = 100
+one = b"GGTGCAGAGCTC" * 8 + b"ACGT"
+est, ok = C.c_uint32(), C.c_int()
+for small in ("1", "0"):
+    os.environ["PF_SMALL"] = small
+    print(f"pf_shouji_filter_one m=100 e=5 (PF_SMALL={small})", bench(lambda: L.lib.pf_shouji_filter_one(
+        ctx.handle, one, len(one), one, len(one), 5, 4, C.byref(ok), C.byref(est), None,
+        C.byref(err)), 2000), "us")
+    for k in (16, 64):
+        b = np.frombuffer(one, np.uint8)[None, :].repeat(k, 0).copy()
+        acck = np.zeros((k + 31) // 32, np.uint32)
+        print(f"  batch of {k}", bench(lambda: L.lib.pf_shouji_filter_batch(
+            ctx.handle, b.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p), 100, k, 100, 5,
+            4, acck.ctypes.data_as(C.c_void_p), None, None, C.byref(err)), 1000), "us")
+os.environ.pop("PF_SMALL", None)
