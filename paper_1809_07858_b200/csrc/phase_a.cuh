@@ -51,6 +51,15 @@ __device__ __forceinline__ uint4 load_row16(const uint8_t* p) {
     }
 }
 
+// The same for the chunk straddling m: only the row's own words (byte offset <
+// pitch) are loaded — the last record's bytes past its pitch may be past the end
+// of the caller's array — and the rest read as "AAAA" (masked off anyway).
+__device__ __forceinline__ uint4 load_row16_lim(const uint8_t* p, int nwords) {
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(p);
+    return make_uint4(nwords > 0 ? q[0] : 0x41414141u, nwords > 1 ? q[1] : 0x41414141u,
+                      nwords > 2 ? q[2] : 0x41414141u, nwords > 3 ? q[3] : 0x41414141u);
+}
+
 // Gather columns [col0, col0 + 4*NCG) of rows [row0, row0+32) into plane words:
 // dst[(col*2 + k) * dstride], k = 0 lo, 1 hi, and ndst[col * dstride] (N). Returns nonzero on any
 // illegal byte. EDGE: the chunk straddles m (bytes at columns >= m are
@@ -80,6 +89,9 @@ __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq
             for (int q = 0; q < 4; ++q) O[cg][k][q] = 0u;
     uint32_t orr = 0u, andd = ~0u, err = 0u;
     uint32_t cm[NCG];
+    // words of the row at/after col0 that lie within its pitch (EDGE loads only)
+    const long long row_words = (static_cast<long long>(pitch) - col0) / 4;
+    const int edge_words = row_words < 4 ? static_cast<int>(row_words) : 4;
     if (EDGE) {
 #pragma unroll
         for (int cg = 0; cg < NCG; ++cg) {
@@ -99,7 +111,8 @@ __device__ __forceinline__ uint32_t gather_chunk(const uint8_t* __restrict__ seq
         for (int i = 0; i < 8; ++i) {
             const long long row = row0 + 8 * g8 + i;
             if (!CHECK_ROWS || row < n)
-                v[i] = load_row16<ALIGN>(seq + row * pitch + col0);  // global or shared
+                v[i] = EDGE ? load_row16_lim(seq + row * pitch + col0, edge_words)
+                            : load_row16<ALIGN>(seq + row * pitch + col0);  // global or shared
             else
                 v[i] = make_uint4(0x41414141u, 0x41414141u, 0x41414141u, 0x41414141u);
         }
