@@ -88,6 +88,13 @@ int pf_device_count(void);
 int pf_ctx_create(const int* devices, int count, pf_ctx** out);
 void pf_ctx_destroy(pf_ctx* ctx);
 int pf_ctx_device_count(const pf_ctx* ctx);
+/* How host batches are spread over the ctx's devices: chunk_pairs = 0 (default)
+ * cuts each batch into one contiguous 32-pair-aligned shard per device (the
+ * n*t/T split of parallel_for_pairs, proj/src/evaluate.cpp:36-37); > 0 deals
+ * consecutive chunks of that many pairs (rounded up to 32) round-robin, chunk c
+ * to device c mod N — BASELINE config 4's streaming layout (1Mi-pair chunks over
+ * 8 GPUs). Results are identical either way. */
+int pf_ctx_set_shard_chunk(pf_ctx* ctx, size_t chunk_pairs);
 
 /* Batched Shouji over caller-owned HOST buffers (pinned or pageable; pinned
  * buffers are DMA'd directly). Synchronous. Checks, in the reference's order:

@@ -39,7 +39,7 @@ EXPORTED = [
     "pf_transfer_bytes", "pf_dibit_pitch", "pf_nplane_pitch", "pf_host_pack_dibits",
     "pf_shouji_filter_dibits_device", "pf_shouji_profile_stages", "pf_magnet_filter_batch", "pf_magnet_filter_device",
     "pf_magnet_filter_one", "pf_packed_words", "pf_shouji_filter_packed_batch",
-    "pf_shouji_filter_packed_device", "pf_host_read_bandwidth",
+    "pf_shouji_filter_packed_device", "pf_host_read_bandwidth", "pf_ctx_set_shard_chunk",
 ]
 
 
@@ -112,6 +112,7 @@ def _bind(lib):
                                                      _u32, _vp, _vp, _vp, C.POINTER(PfError)]),
         "pf_transfer_bytes": (None, [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "pf_host_read_bandwidth": (C.c_double, [_vp, _sz, C.c_int]),
+        "pf_ctx_set_shard_chunk": (C.c_int, [_vp, _sz]),
         "pf_packed_words": (_sz, [_u32]),
         "pf_shouji_filter_packed_batch": (C.c_int, [_vp, _vp, _vp, _sz, _u32, _u32, _u32, _vp, _vp,
                                                     _vp, C.POINTER(PfError)]),

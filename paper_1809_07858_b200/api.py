@@ -233,6 +233,11 @@ class Context:
     def device_count(self) -> int:
         return L.lib.pf_ctx_device_count(self._h)
 
+    def set_shard_chunk(self, chunk_pairs: int) -> None:
+        """0: one contiguous shard per device (default); > 0: chunks of that many pairs
+        dealt round-robin over the devices (pf_ctx_set_shard_chunk)."""
+        _raise(L.lib.pf_ctx_set_shard_chunk(self._h, int(chunk_pairs)))
+
     def close(self):
         if self._h:
             L.lib.pf_ctx_destroy(self._h)

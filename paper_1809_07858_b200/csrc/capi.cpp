@@ -101,6 +101,10 @@ struct DeviceState {
 struct pf_ctx {
     std::vector<DeviceState> devs;
     std::mutex mu;
+    // host batches: 0 = one contiguous 32-aligned shard per device (parallel_for_pairs'
+    // split); > 0 = chunks of this many pairs dealt round-robin (chunk c -> device
+    // c mod N), the streamed layout of BASELINE config 4
+    size_t shard_chunk = 0;
 };
 
 namespace {
@@ -963,6 +967,13 @@ void pf_ctx_destroy(pf_ctx* ctx) {
 
 int pf_ctx_device_count(const pf_ctx* ctx) { return ctx ? static_cast<int>(ctx->devs.size()) : 0; }
 
+int pf_ctx_set_shard_chunk(pf_ctx* ctx, size_t chunk_pairs) {
+    if (!ctx) return PF_ERR_NULL_ARGUMENT;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    ctx->shard_chunk = chunk_pairs == 0 ? 0 : (chunk_pairs + 31) / 32 * 32;
+    return PF_OK;
+}
+
 }  // extern "C"
 
 namespace {
@@ -1081,6 +1092,23 @@ void run_packed_shard(DeviceState& d, const uint64_t* text, const uint64_t* patt
                          cudaMemcpyDeviceToHost, d.stream), "D2H bits"))
         return;
     cu(cudaStreamSynchronize(d.stream), "sync");
+}
+
+// Shard boundaries of an n-pair host batch over nd devices: nd contiguous
+// 32-aligned shards (parallel_for_pairs' n*t/T split, evaluate.cpp:36-37), or,
+// with a shard chunk, consecutive chunks that the devices take round-robin
+// (shard k on device k mod nd). Every boundary is a multiple of 32, so bitmap
+// words never straddle devices.
+std::vector<size_t> shard_bounds(size_t n, size_t nd, size_t chunk) {
+    std::vector<size_t> b;
+    if (chunk == 0 || nd == 1) {
+        const size_t groups = (n + 31) / 32;
+        for (size_t t = 0; t <= nd; ++t) b.push_back(std::min(n, groups * t / nd * 32));
+        return b;
+    }
+    for (size_t p = 0; p < n; p += chunk) b.push_back(p);
+    b.push_back(n);
+    return b;
 }
 
 // ---- latency path: small batches ------------------------------------------------
@@ -1212,29 +1240,30 @@ int run_batch(pf_ctx* ctx, const uint8_t* text, const uint8_t* pattern, size_t s
         return run_small(ctx->devs[0], text, pattern, stride, nullptr, nullptr, n, m, e, width,
                          accept_bitmap, estimates, bits, err);
     const size_t nd = ctx->devs.size();
-    // contiguous 32-aligned shards (parallel_for_pairs' n*t/T split, evaluate.cpp:36-37)
-    const size_t groups = (n + 31) / 32;
-    std::vector<size_t> bounds(nd + 1);
-    for (size_t t = 0; t <= nd; ++t) bounds[t] = std::min(n, groups * t / nd * 32);
-    std::vector<ShardResult> res(nd);
+    const std::vector<size_t> bounds = shard_bounds(n, nd, ctx->shard_chunk);
+    const size_t nshards = bounds.size() - 1;
+    std::vector<ShardResult> res(nshards);
+    auto work = [&](size_t t) {  // device t runs shards t, t+nd, ... in order
+        for (size_t k = t; k < nshards; k += nd) {
+            run_host_shard(ctx->devs[t], text, pattern, stride, bounds[k], bounds[k + 1], m, e,
+                           width, accept_bitmap, estimates, bits, dist, magnet, &res[k]);
+            if (res[k].status != PF_OK) break;
+        }
+    };
     if (nd == 1) {
-        run_host_shard(ctx->devs[0], text, pattern, stride, bounds[0], bounds[1], m, e, width,
-                       accept_bitmap, estimates, bits, dist, magnet, &res[0]);
+        work(0);
     } else {
         std::vector<std::thread> pool;
-        for (size_t t = 0; t < nd; ++t)
-            pool.emplace_back(run_host_shard, std::ref(ctx->devs[t]), text, pattern, stride,
-                              bounds[t], bounds[t + 1], m, e, width, accept_bitmap, estimates, bits,
-                              dist, magnet, &res[t]);
+        for (size_t t = 0; t < nd; ++t) pool.emplace_back(work, t);
         for (auto& th : pool) th.join();
     }
     // First failure in pair order wins (illegal characters are located per
     // shard; shards are in pair order).
-    for (size_t t = 0; t < nd; ++t) {
-        if (res[t].status != PF_OK) {
-            if (err) *err = res[t].err;
-            if (err) err->status = res[t].status;
-            return res[t].status;
+    for (size_t k = 0; k < nshards; ++k) {
+        if (res[k].status != PF_OK) {
+            if (err) *err = res[k].err;
+            if (err) err->status = res[k].status;
+            return res[k].status;
         }
     }
     if (!dist && !magnet && (width < 3 || width > 8)) {  // window_zero_table ctor (shouji.cpp:9-15)
@@ -1347,26 +1376,28 @@ int pf_shouji_filter_packed_batch(pf_ctx* ctx, const uint64_t* text_planes,
         return run_small(ctx->devs[0], nullptr, nullptr, 0, text_planes, pattern_planes, n, m, e,
                          width, accept_bitmap, estimates, bits, err);
     const size_t nd = ctx->devs.size();
-    const size_t groups = (n + 31) / 32;
-    std::vector<size_t> bounds(nd + 1);
-    for (size_t t = 0; t <= nd; ++t) bounds[t] = std::min(n, groups * t / nd * 32);
-    std::vector<ShardResult> res(nd);
+    const std::vector<size_t> bounds = shard_bounds(n, nd, ctx->shard_chunk);
+    const size_t nshards = bounds.size() - 1;
+    std::vector<ShardResult> res(nshards);
+    auto work = [&](size_t t) {
+        for (size_t k = t; k < nshards; k += nd) {
+            run_packed_shard(ctx->devs[t], text_planes, pattern_planes, bounds[k], bounds[k + 1],
+                             m, e, width, accept_bitmap, estimates, bits, &res[k]);
+            if (res[k].status != PF_OK) break;
+        }
+    };
     if (nd == 1) {
-        run_packed_shard(ctx->devs[0], text_planes, pattern_planes, bounds[0], bounds[1], m, e,
-                         width, accept_bitmap, estimates, bits, &res[0]);
+        work(0);
     } else {
         std::vector<std::thread> pool;
-        for (size_t t = 0; t < nd; ++t)
-            pool.emplace_back(run_packed_shard, std::ref(ctx->devs[t]), text_planes,
-                              pattern_planes, bounds[t], bounds[t + 1], m, e, width,
-                              accept_bitmap, estimates, bits, &res[t]);
+        for (size_t t = 0; t < nd; ++t) pool.emplace_back(work, t);
         for (auto& th : pool) th.join();
     }
-    for (size_t t = 0; t < nd; ++t) {
-        if (res[t].status != PF_OK) {
-            if (err) *err = res[t].err;
-            if (err) err->status = res[t].status;
-            return res[t].status;
+    for (size_t k = 0; k < nshards; ++k) {
+        if (res[k].status != PF_OK) {
+            if (err) *err = res[k].err;
+            if (err) err->status = res[k].status;
+            return res[k].status;
         }
     }
     return PF_OK;
