@@ -13,17 +13,22 @@ DESIGN.md "Measurement"):
 * e2e    — the same workload through the public host API
   (pf_shouji_filter_batch) from pinned host ASCII records: the host cores pack
   2-bit records chunk by chunk, H2D, kernels, D2H of the accept bitmap, every
-  step (wall clock, max over ranks); the H2D/D2H bytes are the library's count.
-* roofline — the step's algorithmic bytes (2m ASCII + 1/8 accept bit per
-  pair) over its average launch time, against MEASURED_PEAKS.json hbm_gbs;
-  per_kernel splits the step live (pack vs search, CUDA events between the two
-  launches) into the pack's HBM fraction and the search's fraction of the
-  measured LOP3 lane rate; design_floor is the step time if both kernels ran
-  at those peaks back to back; the BASELINE.md INT formula view is beside it.
+  step (wall clock, max over ranks); the H2D/D2H bytes are the library's count;
+  its bound (the host cores' read rate over the same records) is measured too.
+* roofline — the dominant kernel's (the pack at E=5): SURVEY 8(d)'s algorithmic
+  bytes (2m ASCII + 1/8 accept bit per pair) over its live-measured launch time
+  (CUDA events between the pack and search launches), against
+  MEASURED_PEAKS.json hbm_gbs; `step` is the same over the whole step;
+  `alu_overlap_bound` the ceiling of any overlap of the two stages (ncu ALU-pipe
+  instructions of both kernels at the measured LOP3 rate vs HBM); `serial_floor`
+  the two kernels back to back at their own peaks; the BASELINE.md INT formula
+  view is beside it.
 * cpu_baseline — the unmodified reference library (oracle/_ref) on this host's
   cores over a bounded sample of the same records (rank 0, N=1 only).
 
-``--impl reference`` runs only the reference CPU path (rank 0) and prints its line.
+``--impl reference`` runs only the reference CPU path (rank 0) on a prefix of the
+same bytes under the same config object and prints its line. ``--gpus N`` outside
+torchrun re-launches under torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
