@@ -91,6 +91,17 @@ struct DeviceState {
     size_t small_out_bytes = 0;
     unsigned* d_small_counter = nullptr;  // CTA completion count (device)
     unsigned small_seq = 0;
+    // hybrid upload (raw ASCII chunks DMA'd from pinned records alongside the
+    // host-pack route): its stream, double-buffered device records, events,
+    // plane scratch and validation flag
+    cudaStream_t raw_stream = nullptr;
+    uint8_t* d_raw[2] = {nullptr, nullptr};
+    size_t d_raw_bytes[2] = {0, 0};
+    cudaEvent_t raw_ev[2] = {nullptr, nullptr};
+    cudaEvent_t raw_done = nullptr;
+    uint32_t* d_raw_scratch = nullptr;
+    size_t raw_scratch_words = 0;
+    uint32_t* d_raw_flag = nullptr;
     // SM-partitioned pack | search pipeline (split.cpp), created on first use
     sb::SplitPipe* split = nullptr;
     int split_sms = -1;  // pack SMs the pipe was built for (-1: none tried)
@@ -261,6 +272,16 @@ long long host_chunk() {
     return v;
 }
 
+// Hybrid upload: when the host records are pinned, a second route DMAs raw
+// ASCII chunks straight from them (200 B/pair of PCIe, no host CPU, device-side
+// validation + pack) while the host cores pack the other chunks to dibits; the
+// two routes take chunks from one counter, so each runs at its own pace.
+// PF_HYBRID=1 turns it on (read per call; A/B runs).
+bool hybrid_enabled() {
+    const char* e = std::getenv("PF_HYBRID");
+    return e && e[0] == '1';
+}
+
 void set_illegal(pf_error* err, uint64_t pair, uint32_t field, uint64_t pos, uint8_t byte) {
     if (!err) return;
     err->status = PF_ERR_ILLEGAL_CHARACTER;
@@ -413,12 +434,109 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         const uint8_t* psrc0 = pattern + p0 * stride;
         if (!cu(scratch_acquire(d, d.stream), "scratch order")) return;
         const long long nchunks = (static_cast<long long>(n) + chunk - 1) / chunk;
-        for (long long i = 0; i < nchunks; ++i) {
-            const int b = static_cast<int>(i & 1);
+        // ---- hybrid: the raw-ASCII route on its own thread and stream ----------------
+        const bool hybrid = !magnet && pinned && stride % 4 == 0 && nchunks >= 2 &&
+                            hybrid_enabled() && sb::use_fused(width, e, static_cast<int>(m));
+        std::atomic<long long> next_chunk{0};
+        std::atomic<bool> stop{false};
+        cudaError_t raw_err = cudaSuccess;
+        std::thread raw_thread;
+        if (hybrid) {
+            const size_t rbytes = 2 * static_cast<size_t>(chunk) * stride;
+            for (int b = 0; b < 2; ++b) {
+                if (!cu(grow(d.d_raw[b], d.d_raw_bytes[b], rbytes), "alloc raw records")) return;
+                if (!d.raw_ev[b] &&
+                    !cu(cudaEventCreateWithFlags(&d.raw_ev[b], cudaEventDisableTiming), "event"))
+                    return;
+            }
+            if (!d.raw_stream &&
+                !cu(cudaStreamCreateWithFlags(&d.raw_stream, cudaStreamNonBlocking), "raw stream"))
+                return;
+            if (!d.raw_done &&
+                !cu(cudaEventCreateWithFlags(&d.raw_done, cudaEventDisableTiming), "event"))
+                return;
+            if (!cu(grow(d.d_raw_scratch, d.raw_scratch_words, sb::planes_scratch_words(chunk, m)),
+                    "alloc raw planes"))
+                return;
+            if (!d.d_raw_flag && !cu(cudaMalloc(&d.d_raw_flag, sizeof(uint32_t)), "alloc flag"))
+                return;
+            if (!cu(cudaStreamWaitEvent(d.raw_stream, d.up_ev, 0), "raw stream order") ||
+                !cu(cudaMemsetAsync(d.d_raw_flag, 0, sizeof(uint32_t), d.raw_stream), "memset flag"))
+                return;
+            raw_thread = std::thread([&] {
+                cudaError_t st = cudaSetDevice(d.device);
+                for (long long k = 0; st == cudaSuccess && !stop.load(); ++k) {
+                    const int b = static_cast<int>(k & 1);
+                    // device buffer b is free once the kernels of this route's chunk k-2 are done
+                    if (k >= 2 && (st = cudaEventSynchronize(d.raw_ev[b])) != cudaSuccess) break;
+                    const long long i = next_chunk.fetch_add(1);
+                    if (i >= nchunks) break;
+                    const long long lo = i * chunk;
+                    const long long cn = std::min<long long>(chunk, static_cast<long long>(n) - lo);
+                    uint8_t* dt = d.d_raw[b];
+                    uint8_t* dq = d.d_raw[b] + static_cast<size_t>(chunk) * stride;
+                    const size_t bytes = static_cast<size_t>(cn - 1) * stride + m;
+                    if ((st = xfer(dt, tsrc0 + lo * stride, bytes, cudaMemcpyHostToDevice,
+                                   d.raw_stream)) != cudaSuccess ||
+                        (st = xfer(dq, psrc0 + lo * stride, bytes, cudaMemcpyHostToDevice,
+                                   d.raw_stream)) != cudaSuccess)
+                        break;
+                    if (stride > m &&  // the last record's padding is read, never used
+                        ((st = cudaMemsetAsync(dt + bytes, 'A', stride - m, d.raw_stream)) != cudaSuccess ||
+                         (st = cudaMemsetAsync(dq + bytes, 'A', stride - m, d.raw_stream)) != cudaSuccess))
+                        break;
+                    sb::FilterArgs ra{};
+                    ra.text = dt;
+                    ra.pattern = dq;
+                    ra.pitch = stride;
+                    ra.n = cn;
+                    ra.m = static_cast<int>(m);
+                    ra.e = e;
+                    ra.width = width;
+                    ra.accept = d.d_accept + lo / 32;
+                    ra.estimates = estimates ? d.d_est + lo : nullptr;
+                    ra.err_flag = d.d_raw_flag;
+                    ra.planes = d.d_raw_scratch;
+                    ra.planes_words = d.raw_scratch_words;
+                    if ((st = sb::launch_filter(ra, d.raw_stream)) != cudaSuccess ||
+                        (st = cudaEventRecord(d.raw_ev[b], d.raw_stream)) != cudaSuccess)
+                        break;
+                }
+                if (st == cudaSuccess) st = cudaEventRecord(d.raw_done, d.raw_stream);
+                raw_err = st;
+            });
+        }
+        // The first illegal byte in pair order, whichever route met it: the host's
+        // exact check over the whole shard (errors only).
+        auto report_first_bad = [&]() {
+            stop.store(true);
+            if (raw_thread.joinable()) raw_thread.join();
+            cudaStreamSynchronize(d.stream);
+            if (d.raw_stream) cudaStreamSynchronize(d.raw_stream);
+            sb::HostBad bad;
+            sb::host_validate_parallel(tsrc0, psrc0, stride, static_cast<long long>(n),
+                                       static_cast<int>(m), &bad);
+            if (bad.any)
+                set_illegal(err, p0 + bad.pair, static_cast<uint32_t>(bad.field),
+                            static_cast<uint64_t>(bad.pos), bad.byte);
+            fail(PF_ERR_ILLEGAL_CHARACTER);
+        };
+        struct JoinGuard {  // never leave the raw thread running on an early return
+            std::thread& t;
+            std::atomic<bool>& stop;
+            ~JoinGuard() {
+                stop.store(true);
+                if (t.joinable()) t.join();
+            }
+        } join_guard{raw_thread, stop};
+        for (long long k = 0;; ++k) {
+            const long long i = hybrid ? next_chunk.fetch_add(1) : k;
+            if (i >= nchunks) break;
+            const int b = static_cast<int>(k & 1);
             const long long lo = i * chunk;
             const long long cn = std::min<long long>(chunk, static_cast<long long>(n) - lo);
-            // the DMA that last read these pinned buffers (chunk i-2) must be done
-            if (i >= 2 && !cu(cudaEventSynchronize(d.nib_ev[b]), "record buffer wait")) return;
+            // the DMA that last read these pinned buffers (chunk k-2 of this route) must be done
+            if (k >= 2 && !cu(cudaEventSynchronize(d.nib_ev[b]), "record buffer wait")) return;
             uint8_t* ht = d.h_nib[b];
             uint8_t* hq = ht + static_cast<size_t>(chunk) * rp;
             uint8_t* hnt = dib ? d.h_nrow[b] : nullptr;
@@ -431,15 +549,17 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             else
                 sb::host_pack_nibbles_parallel(tsrc0 + lo * stride, psrc0 + lo * stride, stride, cn,
                                                static_cast<int>(m), ht, hq, &bad);
-            if (bad.any) {  // chunks run in pair order: the first chunk with a bad byte wins
+            if (bad.any) {
+                if (hybrid) return report_first_bad();  // the other route may hold an earlier one
+                // one route: chunks run in pair order, the first chunk with a bad byte wins
                 cu(cudaStreamSynchronize(d.stream), "sync");
                 set_illegal(err, p0 + lo + bad.pair, static_cast<uint32_t>(bad.field),
                             static_cast<uint64_t>(bad.pos), bad.byte);
                 return fail(PF_ERR_ILLEGAL_CHARACTER);
             }
             const size_t cb = static_cast<size_t>(cn) * rp;
-            // device buffer b is free once chunk i-2's kernels (which read it) are done
-            if (i >= 2 && !cu(cudaStreamWaitEvent(d.copy_stream, d.kern_ev[b], 0), "buffer order"))
+            // device buffer b is free once chunk k-2's kernels (which read it) are done
+            if (k >= 2 && !cu(cudaStreamWaitEvent(d.copy_stream, d.kern_ev[b], 0), "buffer order"))
                 return;
             if (!cu(xfer(d.d_nib[b], ht, cb, cudaMemcpyHostToDevice, d.copy_stream), "H2D records"))
                 return;
@@ -490,6 +610,18 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             a.planes_words = d.scratch_words;
             if (!cu(sb::launch_filter(a, d.stream), "filter kernel")) return;
             if (!cu(cudaEventRecord(d.kern_ev[b], d.stream), "record event")) return;
+        }
+        if (hybrid) {
+            stop.store(false);
+            raw_thread.join();
+            if (!cu(raw_err, "raw route")) return;
+            uint32_t raw_flag = 0;
+            if (!cu(cudaMemcpyAsync(&raw_flag, d.d_raw_flag, sizeof(raw_flag),
+                                    cudaMemcpyDeviceToHost, d.raw_stream), "D2H flag") ||
+                !cu(cudaStreamSynchronize(d.raw_stream), "sync"))
+                return;
+            if (raw_flag) return report_first_bad();
+            if (!cu(cudaStreamWaitEvent(d.stream, d.raw_done, 0), "raw route order")) return;
         }
         if (!cu(scratch_release(d, d.stream), "scratch order")) return;
         if (!cu(xfer(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
@@ -934,6 +1066,17 @@ void pf_ctx_destroy(pf_ctx* ctx) {
         if (d.scratch_ev) cudaEventDestroy(d.scratch_ev);
         sb::split_destroy(d.split);
         d.split = nullptr;
+        if (d.raw_stream) {
+            cudaStreamSynchronize(d.raw_stream);
+            cudaStreamDestroy(d.raw_stream);
+        }
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(d.d_raw[b]);
+            if (d.raw_ev[b]) cudaEventDestroy(d.raw_ev[b]);
+        }
+        if (d.raw_done) cudaEventDestroy(d.raw_done);
+        cudaFree(d.d_raw_scratch);
+        cudaFree(d.d_raw_flag);
         if (d.h_small_in) cudaFreeHost(d.h_small_in);
         if (d.h_small_out) cudaFreeHost(d.h_small_out);
         cudaFree(d.d_small_counter);

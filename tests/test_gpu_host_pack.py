@@ -7,6 +7,8 @@ pf_shouji_filter_batch routes host batches of >= 65536 pairs through this path
 (PF_HOST_PACK unset), so the large-batch tests below exercise it end to end,
 including chunk boundaries (256Ki pairs per chunk) and error order across chunks.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -219,3 +221,41 @@ def test_magnet_host_batch_chunks_and_errors(gpu, oracle):
     with pytest.raises(gpu.illegal_character_error) as ei:
         gpu.magnet_filter_batch(t, p, 6)
     assert (ei.value.pair, ei.value.field, ei.value.position()) == (400_000, 0, 99)
+
+
+@pytest.fixture
+def hybrid_on():
+    os.environ["PF_HYBRID"] = "1"
+    yield
+    os.environ.pop("PF_HYBRID", None)
+
+
+def test_hybrid_upload_routes_match(gpu, oracle, hybrid_on):
+    """PF_HYBRID=1: raw-ASCII chunks DMA'd from the pinned records run alongside the
+    host-packed chunks (two routes taking chunks from one counter); the results must
+    be the single-route results, and an illegal byte anywhere must still be the first
+    one in pair order whichever route met it."""
+    import torch
+    n, m, e = 3_000_000, 100, 5
+    t, p = oracle.gen_config(1, 5150, e, m, 0, n)
+    ht = torch.from_numpy(t).pin_memory().numpy()
+    hp = torch.from_numpy(p).pin_memory().numpy()
+    a1, e1, _ = gpu.shouji_filter_batch(ht, hp, e, estimates=True)
+    os.environ["PF_HYBRID"] = "0"
+    a2, e2, _ = gpu.shouji_filter_batch(ht, hp, e, estimates=True)
+    os.environ["PF_HYBRID"] = "1"
+    assert (a1 == a2).all() and (e1 == e2).all()
+    k = 20_000
+    _, e3, _ = oracle.shouji_batch(t[-k:], p[-k:], e)
+    assert (e1[-k:] == e3).all()
+    for where in [(2_900_001, 1, 99), (262_145, 0, 0), (1_000_000, 1, 50)]:
+        hq = hp.copy() if where[1] else hp
+        hu = ht.copy() if not where[1] else ht
+        hq = torch.from_numpy(hq).pin_memory().numpy()
+        hu = torch.from_numpy(hu).pin_memory().numpy()
+        tgt = hq if where[1] else hu
+        tgt[where[0], where[2]] = ord("z")
+        tgt[2_999_999, 3] = ord("y")  # a later one must not win
+        with pytest.raises(gpu.illegal_character_error) as ex:
+            gpu.shouji_filter_batch(hu, hq, e)
+        assert (ex.value.pair, ex.value.field, ex.value.position()) == where
