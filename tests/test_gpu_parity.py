@@ -591,3 +591,22 @@ def test_sparse_n_groups(gpu, oracle, m):
     t[n - 1, m // 2] = ord("N")        # the ragged last group
     for e in sorted({0, 3, 5, 9, 13, min(m - 1, 25)}):
         check_batch(gpu, oracle, t, p, e)
+
+
+@pytest.mark.parametrize("m", [2047, 2048, 2049, 4095, 4096, 6000])
+def test_very_long_records(gpu, oracle, m):
+    """Records past the blocked kernels' 12-plane counter (m > 4095: the per-column
+    generic kernel) and around the latency kernel's m limit (2048), widths 4 and 6,
+    a few thresholds — against the oracle (throughput path: n = 300 > 64)."""
+    rng = np.random.default_rng(m)
+    n = 300
+    t = np.frombuffer(b"ACGTN", np.uint8)[rng.choice(5, size=(n, m), p=[.2475] * 4 + [.01])]
+    p = t.copy()
+    mask = rng.random((n, m)) < 0.03
+    p[mask] = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=int(mask.sum()))]
+    p[: n // 3, 1:] = t[: n // 3, :-1]
+    for w in (4, 6):
+        for e in (0, 7, 40):
+            check_batch(gpu, oracle, t, p, e, width=w)
+    # and the latency path for the same long records
+    check_batch(gpu, oracle, t[:5], p[:5], 7)
