@@ -67,7 +67,7 @@ __global__ void shouji_small_kernel(SmallArgs a) {
     uint8_t* tc = pc + m + 2 * e + 16;  // text codes; 7 past m
     uint8_t* bs = tc + m + 16;          // best slice per window
     uint8_t* bz = bs + m + 16;          // its zero count
-    uint8_t* bv = bz + m + 16;          // tally bits; 1 past m
+    uint8_t* bv = bz + m + 16;          // tally words (m + 16 bytes)
     __shared__ uint32_t ones_total;
     __shared__ int bad_here;
     if (threadIdx.x == 0) {
@@ -76,10 +76,7 @@ __global__ void shouji_small_kernel(SmallArgs a) {
     }
 
     for (int i = threadIdx.x; i < m + 2 * e + 16; i += blockDim.x) pc[i] = 6;
-    for (int i = threadIdx.x; i < m + 16; i += blockDim.x) {
-        tc[i] = 7;
-        bv[i] = 1;
-    }
+    for (int i = threadIdx.x; i < m + 16; i += blockDim.x) tc[i] = 7;
     __syncthreads();
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
         uint8_t p, t;
@@ -156,32 +153,50 @@ __global__ void shouji_small_kernel(SmallArgs a) {
     // of S = bv[j .. j+w-2] (bit i = column j+i; columns >= m read as 1, the
     // pad of extract(pos, w, pad = 1)). Strict improvement: commit iff
     // zeros(best) > (w-1) - popcount(S); the committed slice's overhang is
-    // dropped (deposit, bitvector.hpp:97-100), i.e. read back as 1.
+    // dropped (deposit, bitvector.hpp:97-100), i.e. read back as 1. Column j's
+    // final bit is decided at step j. The best slices are read 16 windows at a
+    // time ahead of the dependent chain; the tally bits go straight into words.
+    // the tally words reuse bv's bytes (8-byte aligned: ceil(m/64)*8 <= m+9 bytes fit)
+    uint64_t* tally = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(bv) + 7) & ~uintptr_t(7));
     if (threadIdx.x == 0) {
         const unsigned full = (1u << (w - 1)) - 1u;
         unsigned S = full;  // bv starts all ones (shouji.cpp:52)
-        for (int j = 0; j < m; ++j) {
-            const unsigned z = bz[j], sl = bs[j];
-            const bool commit = z + static_cast<unsigned>(__popc(S)) > static_cast<unsigned>(w - 1);
-            // columns j+1 .. j+w-1 after the step; those >= m read as 1
-            const int past = j + w - m;  // columns j+w-1-past+1 .. j+w-1 are past the end
-            const unsigned pad = past > 0 ? (full << (w - 1 - (past < w - 1 ? past : w - 1))) & full
-                                          : 0u;
-            bv[j] = static_cast<uint8_t>(commit ? (sl & 1u) : (S & 1u));
-            S = (commit ? (sl >> 1) : ((S >> 1) | (1u << (w - 2)))) | pad;
-        }
-    }
-    __syncthreads();
-    // tally bits (bitvector words) and the popcount
-    const int W = (m + 63) / 64;
-    for (int k = threadIdx.x; k < W; k += blockDim.x) {
         uint64_t word = 0;
-        for (int b = 0; b < 64 && 64 * k + b < m; ++b)
-            word |= static_cast<uint64_t>(bv[64 * k + b]) << b;
-        if (a.bits) a.bits[static_cast<size_t>(pair) * W + k] = word;
-        atomicAdd(&ones_total, static_cast<uint32_t>(__popcll(word)));
+        uint32_t ones = 0;
+        for (int j0 = 0; j0 < m; j0 += 16) {
+            uint8_t zb[16], sb[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {  // bs / bz have 16 bytes of slack past m
+                zb[k] = bz[j0 + k];
+                sb[k] = bs[j0 + k];
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int j = j0 + k;
+                if (j >= m) break;
+                const unsigned z = zb[k], sl = sb[k];
+                const bool commit = z + static_cast<unsigned>(__popc(S)) > static_cast<unsigned>(w - 1);
+                const unsigned bit = commit ? (sl & 1u) : (S & 1u);
+                S = commit ? (sl >> 1) : ((S >> 1) | (1u << (w - 2)));
+                const int past = j + w - m;  // state columns past the end read as 1
+                if (past > 0)
+                    S |= (full << (w - 1 - (past < w - 1 ? past : w - 1))) & full;
+                word |= static_cast<uint64_t>(bit) << (j & 63);
+                ones += bit;
+                if ((j & 63) == 63 || j == m - 1) {
+                    tally[j >> 6] = word;
+                    word = 0;
+                }
+            }
+        }
+        ones_total = ones;
     }
     __syncthreads();
+    // tally bits (bitvector words)
+    const int W = (m + 63) / 64;
+    if (a.bits)
+        for (int k = threadIdx.x; k < W; k += blockDim.x)
+            a.bits[static_cast<size_t>(pair) * W + k] = tally[k];
     if (threadIdx.x == 0) {
         if (a.est) a.est[pair] = ones_total;
         a.accept[pair] = ones_total <= a.e ? 1 : 0;
