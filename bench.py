@@ -343,7 +343,9 @@ def build_roofline(pf, ctx, dev, rank, n, m, e, pitch, step_ms, kern_avg_ms, sta
         # unless skipped for N-free pair blocks)
         pack_bytes = 2 * m + 2 * 2 * m / 8 + (0 if nflags else 2 * m / 8)
         windows = ((m + 3 + 3) // 4) * 4
-        lop3_pair = ((2 * e + 1) * (6 if nflags else 7) + 2 * e * 10 + 19) * windows / 32
+        # per window and 32-pair group: map 2 (+1 with N planes) + rank key 5 per diagonal,
+        # compare 3 + select 5 per further diagonal, commit + tally 19 (csrc/fused.cuh)
+        lop3_pair = ((2 * e + 1) * (7 if nflags else 8) + 2 * e * 8 + 19) * windows / 32
         per_kernel = [
             {"kernel": f"sb::pack_tile_kernel<8,128,{(pitch // 4) % 4},0,1>", "ms": pk_ms,
              "share": pk_ms / (pk_ms + se_ms), "bound": "hbm",

@@ -37,62 +37,69 @@
 
 namespace sb {
 
-// A window's candidate: the key planes and slice bits 1, 2. The slice's last
-// bit is implied — the low bit of ones is the parity of the four slice bits,
-// so s3 = k1 ^ k0 ^ s1 ^ s2 — and is recovered once per window at commit.
+// A window's candidate. select_window orders candidates by key = 2*ones + s0
+// (more zeros first, then a leading zero); only 8 (ones, s0) combinations
+// exist — ones = 0 forces s0 = 0 and ones = 4 forces s0 = 1 — so the key is
+// held as its 3-bit rank among them:
+//   (ones, s0): (0,0) (1,0) (1,1) (2,0) (2,1) (3,0) (3,1) (4,1)
+//   rank:         0     1     2     3     4     5     6     7
+// which keeps the order (strict first minimum of the rank == of the key) with
+// one plane less to compare and select. The slice is (s0, s1, s2, s3): s0
+// and the parity of ones decode from the rank, s1 and s2 are carried, and s3
+// is implied by the parity — all recovered once per window at commit.
 struct Cand4 {
-    uint32_t k[4];  // key planes: k0 = slice bit 0, k1..k3 = ones count
+    uint32_t r[3];  // rank planes, LSB first
     uint32_t s[2];  // slice bits 1..2
 };
 
 // The four windows of a block over D columns sv[0..6] (window b = sv[b..b+3]).
-// Windows 0,1 share the triple sv[1..3] and windows 2,3 the triple sv[3..5]:
-// ones = triple + the window's outer bit, 4 LOP3 per window instead of 5.
+// Window b's rank from s0 = sv[b] and u = sv[b+1] + sv[b+2] + sv[b+3]
+// (u0 = xor, u1 = majority):
+//   s0 = 0: rank = 2u - [u >= 1]   -> r0 = u1|u0, r1 = u1&~u0, r2 = u1&u0
+//   s0 = 1: rank = 2u + 2 - [u==3] -> r0 = u1&u0, r1 = u1|~u0, r2 = u1|u0
+// i.e. one LOP3 per rank plane: 5 LOP3 per window.
 __device__ __forceinline__ void make_block_cands(const uint32_t (&sv)[7], Cand4 (&cd)[4]) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const uint32_t a = sv[2 * h + 1], b = sv[2 * h + 2], c = sv[2 * h + 3];
-        const uint32_t t0 = lop3<0x96>(a, b, c);  // a ^ b ^ c
-        const uint32_t t1 = lop3<0xE8>(a, b, c);  // majority
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            const int bw = 2 * h + w;
-            const uint32_t x = w == 0 ? sv[2 * h] : sv[2 * h + 4];
-            cd[bw].k[0] = sv[bw];
-            cd[bw].k[1] = t0 ^ x;
-            cd[bw].k[2] = lop3<0x78>(t1, t0, x);  // t1 ^ (t0 & x)
-            cd[bw].k[3] = lop3<0x80>(t1, t0, x);  // t1 & t0 & x
-            cd[bw].s[0] = sv[bw + 1];
-            cd[bw].s[1] = sv[bw + 2];
-        }
+    for (int b = 0; b < 4; ++b) {
+        const uint32_t a = sv[b + 1], c = sv[b + 2], d = sv[b + 3];
+        const uint32_t u0 = lop3<0x96>(a, c, d);  // a ^ c ^ d
+        const uint32_t u1 = lop3<0xE8>(a, c, d);  // majority
+        cd[b].r[0] = lop3<0x8E>(sv[b], u1, u0);  // s0 ? u1&u0 : u1|u0
+        cd[b].r[1] = lop3<0xD4>(sv[b], u1, u0);  // s0 ? u1|~u0 : u1&~u0
+        cd[b].r[2] = lop3<0xE8>(sv[b], u1, u0);  // s0 ? u1|u0 : u1&u0 (majority)
+        cd[b].s[0] = a;
+        cd[b].s[1] = c;
     }
 }
 
-// best = c if key(c) < key(best): 4 LOP3 for the strict compare (LSB first:
-// lt = ~c&b | ~(c^b)&lt, table 0x8E) and 6 for the select (lt ? c : best,
-// table 0xE4) — 10 per candidate, pinned with explicit lop3.
+// best = c if rank(c) < rank(best): 3 LOP3 for the strict compare (LSB first:
+// lt = ~c&b | ~(c^b)&lt, table 0x8E) and 5 for the select (lt ? c : best,
+// table 0xE4) — 8 per candidate, pinned with explicit lop3.
 __device__ __forceinline__ void update_best4(const Cand4& c, Cand4& best) {
-    uint32_t lt = lop3<0x8E>(c.k[0], best.k[0], 0u);
-    lt = lop3<0x8E>(c.k[1], best.k[1], lt);
-    lt = lop3<0x8E>(c.k[2], best.k[2], lt);
-    lt = lop3<0x8E>(c.k[3], best.k[3], lt);
+    uint32_t lt = lop3<0x8E>(c.r[0], best.r[0], 0u);
+    lt = lop3<0x8E>(c.r[1], best.r[1], lt);
+    lt = lop3<0x8E>(c.r[2], best.r[2], lt);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) best.k[i] = lop3<0xE4>(c.k[i], best.k[i], lt);
+    for (int i = 0; i < 3; ++i) best.r[i] = lop3<0xE4>(c.r[i], best.r[i], lt);
 #pragma unroll
     for (int i = 0; i < 2; ++i) best.s[i] = lop3<0xE4>(c.s[i], best.s[i], lt);
 }
 
-// commit_window as a state machine over S = tally bits (j, j+1, j+2).
+// commit_window as a state machine over S = tally bits (j, j+1, j+2). Bit j+3
+// is still 1, so "more zeros than the incumbent" is ones(best) <= p with
+// p = S0+S1+S2, i.e. rank(best) <= 2p (the largest rank with ones = p).
 __device__ __forceinline__ uint32_t fsm_step4(const Cand4& best, uint32_t (&S)[3]) {
-    const uint32_t s3 = lop3<0x96>(best.k[1], best.k[0], best.s[0]) ^ best.s[1];  // ones parity
-    const uint32_t p0 = S[0] ^ S[1] ^ S[2];
-    const uint32_t p1 = (S[0] & S[1]) | (S[0] & S[2]) | (S[1] & S[2]);
-    const uint32_t x0 = ~best.k[1] | p0;
-    const uint32_t x1 = (~best.k[2] & p1) | (~(best.k[2] ^ p1) & x0);
-    const uint32_t commit = ~best.k[3] & x1;
-    const uint32_t out = (commit & best.k[0]) | (~commit & S[0]);
-    S[0] = (commit & best.s[0]) | (~commit & S[1]);
-    S[1] = (commit & best.s[1]) | (~commit & S[2]);
+    const uint32_t r0 = best.r[0], r1 = best.r[1], r2 = best.r[2];
+    const uint32_t s0 = lop3<0xD4>(r2, r1, r0);          // rank in {2,4,6,7}
+    const uint32_t g = lop3<0xB2>(r2, r1, r0);           // parity(ones) ^ s0 = r0^r1^s0
+    const uint32_t s3 = lop3<0x96>(g, best.s[0], best.s[1]);
+    const uint32_t p0 = lop3<0x96>(S[0], S[1], S[2]);
+    const uint32_t p1 = lop3<0xE8>(S[0], S[1], S[2]);
+    const uint32_t le1 = lop3<0x4D>(r1, p0, r0);          // (r1 r0) <= (p0 0)
+    const uint32_t commit = lop3<0x8E>(r2, p1, le1);      // (r2 r1 r0) <= (p1 p0 0)
+    const uint32_t out = lop3<0xE4>(s0, S[0], commit);
+    S[0] = lop3<0xE4>(best.s[0], S[1], commit);
+    S[1] = lop3<0xE4>(best.s[1], S[2], commit);
     S[2] = s3 | ~commit;
     return out;
 }
