@@ -104,7 +104,7 @@ struct DeviceState {
     uint32_t* d_raw_flag = nullptr;
     // SM-partitioned pack | search pipeline (split.cpp), created on first use
     sb::SplitPipe* split = nullptr;
-    int split_sms = -1;  // pack SMs the pipe was built for (-1: none tried)
+    int split_sms = 0;  // PF_SPLIT setting the pipe was built for (0: none tried)
 };
 
 }  // namespace
@@ -197,8 +197,8 @@ bool split_applies(const sb::FilterArgs& a) {
 }
 
 sb::SplitPipe* split_pipe(DeviceState& d) {
-    const int want = split_pack_sms_setting();
-    if (want <= 0) return nullptr;
+    const int want = split_pack_sms_setting();  // < 0: shared mode (split.cpp)
+    if (want == 0) return nullptr;
     if (d.split_sms != want) {
         sb::split_destroy(d.split);
         std::string why;

@@ -16,8 +16,11 @@ namespace {
 // One CTA of NT threads per tile of GROUPS x 32 pairs (pack_one_tile,
 // pack_tile.cuh). NFLAG: also write the N-presence flags (pack.cuh) and skip
 // N-free tiles' N planes. 128 registers: ptxas would otherwise take up to 180.
-template <int GROUPS, int NT, int PM, bool NIB, bool NFLAG = false>
-__global__ void __launch_bounds__(NT, 512 / NT)
+// ICH = 8 (lean): 8-column items, up to IPT per thread, 64 registers (8 CTAs
+// of 128 threads fit the register file, so the pack's CTAs leave room for
+// others on the SM).
+template <int GROUPS, int NT, int PM, bool NIB, bool NFLAG = false, int ICH = CH, int IPT = 1>
+__global__ void __launch_bounds__(NT, (ICH == CH ? 512 : 1024) / NT)
 pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
                  size_t pitch, long long n, int m, uint32_t* __restrict__ planes,
                  uint32_t* __restrict__ err_flag, uint32_t* __restrict__ nflags) {
@@ -30,7 +33,7 @@ pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ p
         for (int i = threadIdx.x; i < static_cast<int>(nzero_words(m)); i += NT) zero[i] = 0u;
     }
     __syncthreads();
-    const uint32_t err = pack_one_tile<PM, NT, NIB, NFLAG>(
+    const uint32_t err = pack_one_tile<PM, NT, NIB, NFLAG, ICH, IPT>(
         sm, &bar, 0, GROUPS, static_cast<long long>(blockIdx.x) * GROUPS, text, pattern, pitch, n, m,
         planes, nflags, sflag);
     if (!NIB && err) atomicOr(err_flag, 1u);
@@ -87,26 +90,45 @@ static TileGeom tile_geom(size_t pitch, int m) {
     return {4, 128};
 }
 
-template <int GROUPS, int NT, int PM, bool NIB = false, bool NFLAG = false>
+template <int GROUPS, int NT, int PM, bool NIB = false, bool NFLAG = false, int ICH = CH, int IPT = 1>
 static cudaError_t launch_tile_f(const uint8_t* text, const uint8_t* pattern, size_t pitch,
                                  long long n, int m, uint32_t* planes, uint32_t* err_flag,
                                  uint32_t* nflags, cudaStream_t s) {
     const cudaError_t st =
-        ensure_smem_attr<pack_tile_kernel<GROUPS, NT, PM, NIB, NFLAG>>(110 * 1024);
+        ensure_smem_attr<pack_tile_kernel<GROUPS, NT, PM, NIB, NFLAG, ICH, IPT>>(110 * 1024);
     if (st != cudaSuccess) return st;
     const long long ngroups = (n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + GROUPS - 1) / GROUPS);
-    pack_tile_kernel<GROUPS, NT, PM, NIB, NFLAG><<<grid, NT, tile_smem(pitch, GROUPS), s>>>(
+    pack_tile_kernel<GROUPS, NT, PM, NIB, NFLAG, ICH, IPT><<<grid, NT, tile_smem(pitch, GROUPS), s>>>(
         text, pattern, pitch, n, m, planes, err_flag, nflags);
     return cudaGetLastError();
+}
+
+// The lean pack (4- or 8-column items, 64 registers) for the 8 x 128 geometry
+// (m <= 128: at most 4 / 2 items per thread): PF_PACK_LEAN=4 or 8.
+static int pack_lean() {
+    static const int cols = [] {
+        const char* e = std::getenv("PF_PACK_LEAN");
+        const int v = e ? std::atoi(e) : 0;
+        return v == 4 || v == 8 ? v : 0;
+    }();
+    return cols;
 }
 
 template <int PM, bool NIB = false, bool NFLAG = false>
 static cudaError_t launch_tile_nt(const uint8_t* text, const uint8_t* pattern, size_t pitch,
                                   long long n, int m, TileGeom tg, uint32_t* planes,
                                   uint32_t* err_flag, uint32_t* nflags, cudaStream_t s) {
-    if (tg.groups == 8)
+    if (tg.groups == 8) {
+        if constexpr (!NIB)
+            if (pack_lean() && m <= 128)
+                return pack_lean() == 4
+                           ? launch_tile_f<8, 128, PM, false, NFLAG, 4, 4>(text, pattern, pitch, n, m,
+                                                                         planes, err_flag, nflags, s)
+                           : launch_tile_f<8, 128, PM, false, NFLAG, 8, 2>(text, pattern, pitch, n, m,
+                                                                         planes, err_flag, nflags, s);
         return launch_tile_f<8, 128, PM, NIB, NFLAG>(text, pattern, pitch, n, m, planes, err_flag, nflags, s);
+    }
     if (tg.nt == 96)
         return launch_tile_f<4, 96, PM, NIB, NFLAG>(text, pattern, pitch, n, m, planes, err_flag, nflags, s);
     return launch_tile_f<4, 128, PM, NIB, NFLAG>(text, pattern, pitch, n, m, planes, err_flag, nflags, s);

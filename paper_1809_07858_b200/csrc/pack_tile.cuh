@@ -59,7 +59,7 @@ __host__ __device__ inline size_t seq_stride(size_t pitch, int groups) {
 }
 inline size_t tile_smem(size_t pitch, int groups) { return 2 * seq_stride(pitch, groups) + 128; }
 
-template <bool EDGE, int PM, bool NIB = false, bool DEFER_N = false>
+template <bool EDGE, int PM, bool NIB = false, bool DEFER_N = false, int MAXNCG = 4>
 __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size_t pitch, int col0,
                                                int m, uint32_t* dst, uint32_t* ndst, int stride,
                                                uint32_t* nout = nullptr) {
@@ -72,11 +72,18 @@ __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size
         }
         return 0u;
     }
-    switch (ncg) {
-        case 1: return gather_chunk_smem<EDGE, 1, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
-        case 2: return gather_chunk_smem<EDGE, 2, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
-        case 3: return gather_chunk_smem<EDGE, 3, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
-        default: return gather_chunk_smem<EDGE, 4, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+    if constexpr (MAXNCG == 1) {
+        return gather_chunk_smem<EDGE, 1, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+    } else if constexpr (MAXNCG == 2) {
+        if (ncg == 1) return gather_chunk_smem<EDGE, 1, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+        return gather_chunk_smem<EDGE, 2, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+    } else {
+        switch (ncg) {
+            case 1: return gather_chunk_smem<EDGE, 1, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+            case 2: return gather_chunk_smem<EDGE, 2, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+            case 3: return gather_chunk_smem<EDGE, 3, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+            default: return gather_chunk_smem<EDGE, 4, PM, DEFER_N>(src, pitch, col0, m, dst, ndst, stride, nout);
+        }
     }
 }
 
@@ -89,7 +96,9 @@ __device__ __forceinline__ uint32_t gather_ncg(int ncg, const uint8_t* src, size
 // N planes only when one of the tile's records of that sequence holds an N;
 // needs one item per thread (2 * GROUPS * ceil(m/16) <= NT) and sflag, 2 words
 // of shared memory.
-template <int PM, int NT, bool NIB = false, bool NFLAG = false>
+// ICH: columns per item (16, or 8 for the lean form: half the accumulator
+// registers per thread, up to IPT items per thread).
+template <int PM, int NT, bool NIB = false, bool NFLAG = false, int ICH = CH, int IPT = 1>
 __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, uint32_t parity,
                                                   int GROUPS, long long g0,
                                                   const uint8_t* __restrict__ text,
@@ -145,53 +154,69 @@ __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, ui
         }
         __syncthreads();
     }
-    // Items are (chunk, group, sequence) tiles of 32 pairs x 16 columns, the
+    // Items are (chunk, group, sequence) tiles of 32 pairs x ICH columns, the
     // sequence fastest. Full chunks come first and the one chunk straddling m
     // (if any) last, so no warp mixes the gather variants.
-    const int C = (mc + CH - 1) / CH;
-    const int Cfull = m / CH;  // chunks entirely inside [0, m)
+    static_assert(ICH == CH || ((ICH == 8 || ICH == 4) && !NIB), "lean items are 4 or 8 columns of ASCII records");
+    const int C = (mc + ICH - 1) / ICH;
+    const int Cfull = m / ICH;  // chunks entirely inside [0, m)
     uint32_t err = 0u;
-    uint32_t sink[CH * 3];
-    uint32_t nw[CH];        // NFLAG: this thread's item's N-plane words
-    uint32_t* ndst = nullptr;
-    int nseq = 0, ncols = 0;
-    for (int it = threadIdx.x; it < 2 * GROUPS * C; it += NT) {
+    uint32_t sink[ICH * 3];
+    uint32_t nw[IPT][ICH];  // NFLAG: this thread's items' N-plane words
+    uint32_t* ndst[IPT];
+    int nseq[IPT], ncols[IPT];
+    const int items = 2 * GROUPS * C;
+    // one item; nwk: its N-plane words (NFLAG), returns the N destination
+    auto do_item = [&](int it, uint32_t* nwk, int& sq_out, int& ncols_out) -> uint32_t* {
         const int c = it / (2 * GROUPS);
         const int g = (it / 2) % GROUPS;
         const int sq = it % 2;
-        uint32_t* dst = planes ? planes + lohi_index(sq, g0 + g, c * CH, 0, nblocks, mc) : sink;
-        uint32_t* nd = planes ? planes + nplane_index(sq, g0 + g, c * CH, nblocks, mc) : sink + 2 * CH;
+        uint32_t* dst = planes ? planes + lohi_index(sq, g0 + g, c * ICH, 0, nblocks, mc) : sink;
+        uint32_t* nd = planes ? planes + nplane_index(sq, g0 + g, c * ICH, nblocks, mc) : sink + 2 * ICH;
         const int stride = planes ? kPackGroups : 1;
         if constexpr (NFLAG) {  // an edge chunk's gather fills only its first 4*ncg words
 #pragma unroll
-            for (int col = 0; col < CH; ++col) nw[col] = 0u;
+            for (int col = 0; col < ICH; ++col) nwk[col] = 0u;
         }
         if (c < Cfull) {
             if constexpr (NIB)
-                gather_chunk_nib<false, 4, NFLAG>(rec(sq, g), pitch, c * CH, m, dst, nd, stride, nw);
+                gather_chunk_nib<false, 4, NFLAG>(rec(sq, g), pitch, c * ICH, m, dst, nd, stride, nwk);
             else
-                err |= gather_chunk_smem<false, 4, PM, NFLAG>(rec(sq, g), pitch, c * CH, m, dst, nd,
-                                                                stride, nw);
+                err |= gather_chunk_smem<false, ICH / 4, PM, NFLAG>(rec(sq, g), pitch, c * ICH, m,
+                                                                    dst, nd, stride, nwk);
         } else {
-            err |= gather_ncg<true, PM, NIB, NFLAG>((m - c * CH + 3) / 4, rec(sq, g), pitch,
-                                                       c * CH, m, dst, nd, stride, nw);
+            err |= gather_ncg<true, PM, NIB, NFLAG, ICH / 4>((m - c * ICH + 3) / 4, rec(sq, g), pitch,
+                                                       c * ICH, m, dst, nd, stride, nwk);
         }
         if constexpr (NFLAG) {
             uint32_t any = 0u;
 #pragma unroll
-            for (int col = 0; col < CH; ++col) any |= nw[col];
+            for (int col = 0; col < ICH; ++col) any |= nwk[col];
             if (any) sflag[sq] = 1u;
-            ndst = nd;
-            nseq = sq;
-            ncols = c < Cfull ? CH : m - c * CH;
         }
+        sq_out = sq;
+        ncols_out = c < Cfull ? ICH : m - c * ICH;
+        return nd;
+    };
+    if constexpr (NFLAG) {  // at most IPT items per thread (checked by the launcher)
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+            const int it = threadIdx.x + k * NT;
+            ndst[k] = it < items ? do_item(it, nw[k], nseq[k], ncols[k]) : nullptr;
+        }
+    } else {
+        int sq_, nc_;
+        for (int it = threadIdx.x; it < items; it += NT) do_item(it, nw[0], sq_, nc_);
     }
     if constexpr (NFLAG) {
         __syncthreads();
-        if (ndst != nullptr && sflag[nseq]) {
 #pragma unroll
-            for (int col = 0; col < CH; ++col)
-                if (col < ncols) ndst[col * kNColWords] = nw[col];
+        for (int k = 0; k < IPT; ++k) {
+            if (ndst[k] != nullptr && sflag[nseq[k]]) {
+#pragma unroll
+                for (int col = 0; col < ICH; ++col)
+                    if (col < ncols[k]) ndst[k][col * kNColWords] = nw[k][col];
+            }
         }
         if (threadIdx.x < 2 * GROUPS) {
             const int sq = threadIdx.x / GROUPS, g = threadIdx.x % GROUPS;

@@ -75,16 +75,25 @@ const Driver& driver() {
 
 }  // namespace
 
+// Shared mode (pack_sms < 0): no partition — one pack stream (chunks packed
+// one after another) and two search streams on the whole device, the pack
+// stream at the higher priority, and a ring of kRing plane buffers, so the
+// block scheduler can place pack CTAs (shared-memory bound) and search CTAs
+// (register bound) on the same SMs.
+constexpr int kRing = 3;
+
 struct SplitPipe {
     int device = 0;
+    bool shared = false;
+    int nbuf = 2;
     CUgreenCtx green[2] = {nullptr, nullptr};  // 0 pack, 1 search
-    cudaStream_t ps[2] = {nullptr, nullptr};   // pack streams (chunk parity)
-    cudaStream_t ss[2] = {nullptr, nullptr};   // search streams
+    cudaStream_t ps[kRing] = {nullptr, nullptr, nullptr};  // pack streams (by buffer)
+    cudaStream_t ss[kRing] = {nullptr, nullptr, nullptr};  // search streams
     cudaEvent_t in_ev = nullptr;
-    cudaEvent_t packed[2] = {nullptr, nullptr};
-    cudaEvent_t searched[2] = {nullptr, nullptr};
-    bool searched_valid[2] = {false, false};
-    uint32_t* planes[2] = {nullptr, nullptr};
+    cudaEvent_t packed[kRing] = {nullptr, nullptr, nullptr};
+    cudaEvent_t searched[kRing] = {nullptr, nullptr, nullptr};
+    bool searched_valid[kRing] = {false, false, false};
+    uint32_t* planes[kRing] = {nullptr, nullptr, nullptr};
     size_t planes_words = 0;
     int pack_sms = 0, search_sms = 0;
 };
@@ -95,16 +104,22 @@ int split_search_sms(const SplitPipe* p) { return p ? p->search_sms : 0; }
 void split_destroy(SplitPipe* p) {
     if (!p) return;
     const Driver& drv = driver();
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kRing; ++b) {
         if (p->ps[b]) cudaStreamSynchronize(p->ps[b]);
         if (p->ss[b]) cudaStreamSynchronize(p->ss[b]);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kRing; ++b) {
         if (p->packed[b]) cudaEventDestroy(p->packed[b]);
         if (p->searched[b]) cudaEventDestroy(p->searched[b]);
         cudaFree(p->planes[b]);
-        if (p->ps[b]) cudaStreamDestroy(p->ps[b]);
-        if (p->ss[b]) cudaStreamDestroy(p->ss[b]);
+        // shared mode aliases streams across buffers: destroy each once
+        bool first_ps = true, first_ss = true;
+        for (int c = 0; c < b; ++c) {
+            if (p->ps[c] == p->ps[b]) first_ps = false;
+            if (p->ss[c] == p->ss[b]) first_ss = false;
+        }
+        if (p->ps[b] && first_ps) cudaStreamDestroy(p->ps[b]);
+        if (p->ss[b] && first_ss) cudaStreamDestroy(p->ss[b]);
     }
     if (p->in_ev) cudaEventDestroy(p->in_ev);
     for (auto g : p->green)
@@ -119,6 +134,36 @@ SplitPipe* split_create(int device, int pack_sms, std::string* why) {
         split_destroy(p);
         return nullptr;
     };
+    if (pack_sms < 0) {  // shared mode: plain priority streams on the whole device
+        auto* p = new SplitPipe;
+        p->device = device;
+        p->shared = true;
+        const char* nb = std::getenv("PF_SPLIT_BUFS");
+        p->nbuf = nb && std::atoi(nb) == 2 ? 2 : kRing;
+        int lo = 0, hi = 0;  // numerically: lo = least priority, hi = greatest
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return fail("priority range", p);
+        const char* pr = std::getenv("PF_SPLIT_PRIO");  // "search": search streams first
+        const bool search_first = pr && std::strcmp(pr, "search") == 0;
+        const int pp = search_first ? lo : hi, sp = search_first ? hi : lo;
+        cudaStream_t pack = nullptr, srch[2] = {nullptr, nullptr};
+        if (cudaStreamCreateWithPriority(&pack, cudaStreamNonBlocking, pp) != cudaSuccess)
+            return fail("cudaStreamCreateWithPriority", p);
+        for (int b = 0; b < kRing; ++b) p->ps[b] = pack;
+        for (int k = 0; k < 2; ++k)
+            if (cudaStreamCreateWithPriority(&srch[k], cudaStreamNonBlocking, sp) != cudaSuccess)
+                return fail("cudaStreamCreateWithPriority", p);
+        for (int b = 0; b < kRing; ++b) p->ss[b] = srch[b & 1];
+        for (int b = 0; b < kRing; ++b)
+            if (cudaEventCreateWithFlags(&p->packed[b], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&p->searched[b], cudaEventDisableTiming) != cudaSuccess)
+                return fail("cudaEventCreate", p);
+        if (cudaEventCreateWithFlags(&p->in_ev, cudaEventDisableTiming) != cudaSuccess)
+            return fail("cudaEventCreate", p);
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        p->pack_sms = p->search_sms = sms;
+        return p;
+    }
     if (!drv.ok) return fail("green-context driver entry points unavailable", nullptr);
     auto* p = new SplitPipe;
     p->device = device;
@@ -160,8 +205,9 @@ SplitPipe* split_create(int device, int pack_sms, std::string* why) {
 cudaError_t split_launch(SplitPipe* p, const FilterArgs& a, cudaStream_t s, long long chunk) {
     chunk = (chunk + 4095) / 4096 * 4096;  // whole search CTAs (4096 pairs) and bitmap words
     const size_t words = planes_scratch_words(chunk, a.m);
+    const int nbuf = p->nbuf;
     if (words > p->planes_words) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < nbuf; ++b) {
             if (p->searched_valid[b]) {
                 const cudaError_t st = cudaEventSynchronize(p->searched[b]);
                 if (st != cudaSuccess) return st;
@@ -170,7 +216,7 @@ cudaError_t split_launch(SplitPipe* p, const FilterArgs& a, cudaStream_t s, long
             p->planes[b] = nullptr;
         }
         p->planes_words = 0;
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < nbuf; ++b) {
             const cudaError_t st = cudaMalloc(&p->planes[b], words * sizeof(uint32_t));
             if (st != cudaSuccess) return st;
         }
@@ -178,14 +224,14 @@ cudaError_t split_launch(SplitPipe* p, const FilterArgs& a, cudaStream_t s, long
     }
     cudaError_t st = cudaEventRecord(p->in_ev, s);  // inputs (and outputs) ready on s
     if (st != cudaSuccess) return st;
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < nbuf; ++b) {
         if ((st = cudaStreamWaitEvent(p->ps[b], p->in_ev, 0)) != cudaSuccess) return st;
         if ((st = cudaStreamWaitEvent(p->ss[b], p->in_ev, 0)) != cudaSuccess) return st;
     }
-    bool used[2] = {false, false};
+    bool used[kRing] = {false, false, false};
     long long i = 0;
     for (long long p0 = 0; p0 < a.n; p0 += chunk, ++i) {
-        const int b = static_cast<int>(i & 1);
+        const int b = static_cast<int>(i % nbuf);
         FilterArgs c = a;
         c.n = std::min<long long>(chunk, a.n - p0);
         c.text = a.text + static_cast<size_t>(p0) * a.pitch;
@@ -206,7 +252,7 @@ cudaError_t split_launch(SplitPipe* p, const FilterArgs& a, cudaStream_t s, long
         p->searched_valid[b] = true;
         used[b] = true;
     }
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < nbuf; ++b)
         if (used[b] && (st = cudaStreamWaitEvent(s, p->searched[b], 0)) != cudaSuccess) return st;
     return cudaSuccess;
 }
