@@ -347,7 +347,7 @@ def build_roofline(pf, ctx, dev, rank, n, m, e, pitch, step_ms, kern_avg_ms, sta
         # compare 3 + select 5 per further diagonal, commit + tally 19 (csrc/fused.cuh)
         lop3_pair = ((2 * e + 1) * (7 if nflags else 8) + 2 * e * 8 + 19) * windows / 32
         per_kernel = [
-            {"kernel": f"sb::pack_tile_kernel<8,128,{(pitch // 4) % 4},0,1>", "ms": pk_ms,
+            {"kernel": f"sb::pack_tile_kernel<8,128,{(pitch // 4) % 4},0,1,16,1>", "ms": pk_ms,
              "share": pk_ms / (pk_ms + se_ms), "bound": "hbm",
              "algorithmic_bytes_per_pair": B,
              "achieved": B * n / (pk_ms * 1e-3) / 1e9, "unit": "GB/s",
