@@ -221,12 +221,13 @@ __device__ __forceinline__ void lds_words(const uint8_t* p, int mis, uint32_t (&
 // 8x8 byte-lane transpose (24 FMA + 24 LOP3) turns the 8 row words into the 8
 // bit planes of the ASCII bytes; bits 1/2/3 are the lo/hi/N planes and all
 // eight check the alphabet (7 LOP3, see the header).
-template <bool EDGE, int NCG, int PM, bool DEFER_N = false>
-__device__ __forceinline__ uint32_t gather_chunk_smem(const uint8_t* __restrict__ seq, size_t pitch,
-                                                      int col0, int m, uint32_t* __restrict__ dst,
-                                                      uint32_t* __restrict__ ndst, int dstride,
-                                                      uint32_t* __restrict__ nout = nullptr) {
-    uint32_t O[NCG][3][4];
+// The gather itself: O[cg][k][q] = plane k (lo, hi, N) column word of column
+// col0 + 4cg + q (columns >= m read as 'A' when EDGE); returns nonzero on an
+// illegal byte. Shared by the store-to-planes form below and the select-in-pack
+// kernel (select_pack.cu), which keeps the words in registers.
+template <bool EDGE, int NCG, int PM>
+__device__ __forceinline__ uint32_t gather_core_smem(const uint8_t* __restrict__ seq, size_t pitch,
+                                                     int col0, int m, uint32_t (&O)[NCG][3][4]) {
 #pragma unroll
     for (int cg = 0; cg < NCG; ++cg)
 #pragma unroll
@@ -273,6 +274,16 @@ __device__ __forceinline__ uint32_t gather_chunk_smem(const uint8_t* __restrict_
                     O[cg][k][q] = __byte_perm(O[cg][k][q], w[k + 1], 0x0321 | ((4 + q) << 12));
         }
     }
+    return err;
+}
+
+template <bool EDGE, int NCG, int PM, bool DEFER_N = false>
+__device__ __forceinline__ uint32_t gather_chunk_smem(const uint8_t* __restrict__ seq, size_t pitch,
+                                                      int col0, int m, uint32_t* __restrict__ dst,
+                                                      uint32_t* __restrict__ ndst, int dstride,
+                                                      uint32_t* __restrict__ nout = nullptr) {
+    uint32_t O[NCG][3][4];
+    const uint32_t err = gather_core_smem<EDGE, NCG, PM>(seq, pitch, col0, m, O);
 #pragma unroll
     for (int cg = 0; cg < NCG; ++cg)
 #pragma unroll
