@@ -23,7 +23,8 @@ template <int GROUPS, int NT, int PM, bool NIB, bool NFLAG = false, int ICH = CH
 __global__ void __launch_bounds__(NT, (ICH == CH ? 512 : 1024) / NT)
 pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
                  size_t pitch, long long n, int m, uint32_t* __restrict__ planes,
-                 uint32_t* __restrict__ err_flag, uint32_t* __restrict__ nflags) {
+                 uint32_t* __restrict__ err_flag, uint32_t* __restrict__ nflags,
+                 long long pf_groups) {
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint32_t sflag[2];
@@ -35,7 +36,7 @@ pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ p
     __syncthreads();
     const uint32_t err = pack_one_tile<PM, NT, NIB, NFLAG, ICH, IPT>(
         sm, &bar, 0, GROUPS, static_cast<long long>(blockIdx.x) * GROUPS, text, pattern, pitch, n, m,
-        planes, nflags, sflag);
+        planes, nflags, sflag, pf_groups);
     if (!NIB && err) atomicOr(err_flag, 1u);
 }
 
@@ -99,8 +100,20 @@ static cudaError_t launch_tile_f(const uint8_t* text, const uint8_t* pattern, si
     if (st != cudaSuccess) return st;
     const long long ngroups = (n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + GROUPS - 1) / GROUPS);
+    // Each CTA also prefetches into L2 the records of the tile pf_tiles tiles
+    // further on (cp.async.bulk.prefetch.L2), so that CTA's bulk copies wait on L2
+    // rather than DRAM: shorter CTA lifetimes, more record bytes in flight per SM
+    // for the same shared memory. Measured (tools/exp_stages.py, pack ms per 16M /
+    // 16M / 8M pairs at m = 100 / 150 / 250): off 0.631 / 1.086 / 0.928, 100 tiles
+    // 0.589 / 1.090 / 0.868, 200-450 tiles 0.573-0.578 / 1.062-1.065 / 0.853-0.855,
+    // 1200 tiles 0.898 / 1.087 / 1.198 (the prefetched lines no longer survive in
+    // L2). PF_PACK_L2PF overrides the distance (0: off).
+    static const long long pf_tiles = [] {
+        const char* e = std::getenv("PF_PACK_L2PF");
+        return e ? std::atoll(e) : 320ll;
+    }();
     pack_tile_kernel<GROUPS, NT, PM, NIB, NFLAG, ICH, IPT><<<grid, NT, tile_smem(pitch, GROUPS), s>>>(
-        text, pattern, pitch, n, m, planes, err_flag, nflags);
+        text, pattern, pitch, n, m, planes, err_flag, nflags, pf_tiles * GROUPS);
     return cudaGetLastError();
 }
 

@@ -105,7 +105,8 @@ __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, ui
                                                   const uint8_t* __restrict__ pattern, size_t pitch,
                                                   long long n, int m, uint32_t* __restrict__ planes,
                                                   uint32_t* __restrict__ nflags = nullptr,
-                                                  uint32_t* sflag = nullptr) {
+                                                  uint32_t* sflag = nullptr,
+                                                  long long pf_groups = 0) {
     const long long row0 = g0 * 32;
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
     const int rows = static_cast<int>(n - row0 < 32 * GROUPS ? n - row0 : 32 * GROUPS);
@@ -132,6 +133,18 @@ __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, ui
         if (b > 0) {
             const uint8_t* src = (sq == 0 ? text : pattern) + (row0 + 32 * g) * pitch;
             bulk_g2s(rec(sq, g), src, static_cast<uint32_t>(b), bar);
+        }
+    } else if (pf_groups > 0 && threadIdx.x < 4 * GROUPS) {
+        // L2 prefetch of the records a CTA pf_groups groups further on will load,
+        // so its bulk copies wait on L2 instead of DRAM (PF_PACK_L2PF)
+        const int t = threadIdx.x - 2 * GROUPS;
+        const int sq = t / GROUPS, g = t % GROUPS;
+        const long long row = row0 + 32 * (pf_groups + g);
+        if (row + 32 <= n) {
+            const uint8_t* src = (sq == 0 ? text : pattern) + row * pitch;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
+                         "r"(static_cast<uint32_t>(32 * ipitch & ~15))
+                         : "memory");
         }
     }
     mbar_wait(bar, parity);
