@@ -28,15 +28,15 @@ pack_tile_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ p
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint32_t sflag[2];
-    if (threadIdx.x == 0) mbar_init(&bar, 1);
     if (NFLAG && blockIdx.x == 0) {  // the all-zero N column image N-free groups read
         uint32_t* zero = nflags + nflag_words(n);
         for (int i = threadIdx.x; i < static_cast<int>(nzero_words(m)); i += NT) zero[i] = 0u;
     }
-    __syncthreads();
+    // thread 0 initialises and arms the barrier inside pack_one_tile, before its
+    // first __syncthreads (one barrier instead of two per CTA)
     const uint32_t err = pack_one_tile<PM, NT, NIB, NFLAG, ICH, IPT>(
         sm, &bar, 0, GROUPS, static_cast<long long>(blockIdx.x) * GROUPS, text, pattern, pitch, n, m,
-        planes, nflags, sflag, pf_groups);
+        planes, nflags, sflag, pf_groups, true);
     if (!NIB && err) atomicOr(err_flag, 1u);
 }
 

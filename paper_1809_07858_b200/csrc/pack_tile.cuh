@@ -106,7 +106,8 @@ __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, ui
                                                   long long n, int m, uint32_t* __restrict__ planes,
                                                   uint32_t* __restrict__ nflags = nullptr,
                                                   uint32_t* sflag = nullptr,
-                                                  long long pf_groups = 0) {
+                                                  long long pf_groups = 0,
+                                                  bool init_bar = false) {
     const long long row0 = g0 * 32;
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
     const int rows = static_cast<int>(n - row0 < 32 * GROUPS ? n - row0 : 32 * GROUPS);
@@ -121,6 +122,7 @@ __device__ __forceinline__ uint32_t pack_one_tile(uint8_t* sm, uint64_t* bar, ui
         return b & ~15;
     };
     if (threadIdx.x == 0) {
+        if (init_bar) mbar_init(bar, 1);  // a one-tile CTA: init and arm under one barrier
         uint32_t total = 0;
         for (int g = 0; g < GROUPS; ++g) total += 2u * static_cast<uint32_t>(tma_bytes(g));
         mbar_expect_tx(bar, total);
