@@ -46,3 +46,14 @@ def test_bench_two_ranks_plumbing():
     assert j["config"]["global_pairs"] == 2 * 1000000
     # whole-job value = pairs of all ranks / max-over-ranks step time
     assert abs(j["value"] - 2 * 1000000 / (j["ms_per_step"] * 1e-3)) < 1e-6 * j["value"]
+
+
+def test_bench_reference_arm_line():
+    """`--impl reference`: the reference library on the host cores over a prefix of the same
+    configs[1] bytes, the same metric/config keys, e2e with no device copies."""
+    j = _run(["--impl", "reference", "--steps", "1", "--warmup", "1"], timeout=900)
+    assert j["impl"] == "reference"
+    ours = _run(["--steps", "3", "--warmup", "3", "--pairs", "2000000", "--no-cpu", "--no-e2e"])
+    assert j["metric"] == ours["metric"] and j["unit"] == ours["unit"]
+    assert j["value"] > 0 and j["cpu_baseline"]["kind"] in ("reference", "port")
+    assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["d2h_bytes_per_step"] == 0
