@@ -341,12 +341,14 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
     const int hp_mode = host_pack_mode();
     // MAGNET reads the dibit records directly (no pack kernel), so it only
     // needs the dibit format and its own length limit.
+    // The edit distance reads the dibit records directly too (m <= 1024).
     const bool shape_ok =
-        magnet ? host_format_dibit() && sb::magnet_supported(static_cast<int>(m))
-               : width >= 3 && width <= 8 && !bits &&
-                     (host_format_dibit() ? sb::dibit_pack_fits(static_cast<int>(m))
-                                          : sb::nibble_pack_fits(static_cast<int>(m)));
-    const bool host_pack = hp_mode != 0 && !dist && e < m && shape_ok &&
+        dist     ? host_format_dibit() && m <= 1024
+        : magnet ? host_format_dibit() && sb::magnet_supported(static_cast<int>(m))
+                 : width >= 3 && width <= 8 && !bits &&
+                       (host_format_dibit() ? sb::dibit_pack_fits(static_cast<int>(m))
+                                            : sb::nibble_pack_fits(static_cast<int>(m)));
+    const bool host_pack = hp_mode != 0 && e < m && shape_ok &&
                            (hp_mode == 1 || (static_cast<long long>(n) >= kHostPackMin &&
                                              // the portable packer is slower than PCIe
                                              sb::host_pack_uses_simd()));
@@ -426,7 +428,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         if (!cu(cudaEventRecord(d.up_ev, d.stream), "record event") ||
             !cu(cudaStreamWaitEvent(d.copy_stream, d.up_ev, 0), "copy stream order"))
             return;
-        if (!magnet &&
+        if (!magnet && !dist &&
             !cu(grow(d.d_scratch, d.scratch_words, sb::planes_scratch_words(chunk, m)),
                 "alloc planes"))
             return;
@@ -435,7 +437,7 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
         if (!cu(scratch_acquire(d, d.stream), "scratch order")) return;
         const long long nchunks = (static_cast<long long>(n) + chunk - 1) / chunk;
         // ---- hybrid: the raw-ASCII route on its own thread and stream ----------------
-        const bool hybrid = !magnet && pinned && stride % 4 == 0 && nchunks >= 2 &&
+        const bool hybrid = !magnet && !dist && pinned && stride % 4 == 0 && nchunks >= 2 &&
                             hybrid_enabled() && sb::use_fused(width, e, static_cast<int>(m));
         std::atomic<long long> next_chunk{0};
         std::atomic<bool> stop{false};
@@ -579,6 +581,18 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             if (!cu(cudaEventRecord(d.nib_ev[b], d.copy_stream), "record event") ||
                 !cu(cudaStreamWaitEvent(d.stream, d.nib_ev[b], 0), "upload order"))
                 return;
+            if (dist) {
+                if (!cu(sb::launch_edit_distance_dibits(
+                            d.d_nib[b], d.d_nib[b] + static_cast<size_t>(chunk) * rp,
+                            has_n ? d.d_nrow[b] : nullptr,
+                            has_n ? d.d_nrow[b] + static_cast<size_t>(chunk) * npr : nullptr, cn,
+                            static_cast<int>(m), static_cast<int>(std::min<uint32_t>(e, 1u << 30)),
+                            reinterpret_cast<int32_t*>(d.d_est) + lo, d.stream),
+                        "edit distance kernel"))
+                    return;
+                if (!cu(cudaEventRecord(d.kern_ev[b], d.stream), "record event")) return;
+                continue;
+            }
             if (magnet) {
                 if (!cu(sb::launch_magnet_dibits(
                             d.d_nib[b], d.d_nib[b] + static_cast<size_t>(chunk) * rp,
@@ -624,6 +638,13 @@ void run_host_shard(DeviceState& d, const uint8_t* text, const uint8_t* pattern,
             if (!cu(cudaStreamWaitEvent(d.stream, d.raw_done, 0), "raw route order")) return;
         }
         if (!cu(scratch_release(d, d.stream), "scratch order")) return;
+        if (dist) {
+            if (!cu(xfer(dist + p0, d.d_est, n * sizeof(int32_t), cudaMemcpyDeviceToHost, d.stream),
+                    "D2H distances"))
+                return;
+            cu(cudaStreamSynchronize(d.stream), "sync");
+            return;
+        }
         if (!cu(xfer(accept_bitmap + p0 / 32, d.d_accept, ngroups * sizeof(uint32_t),
                                 cudaMemcpyDeviceToHost, d.stream), "D2H accept"))
             return;

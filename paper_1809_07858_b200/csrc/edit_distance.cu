@@ -19,6 +19,7 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "pack.cuh"
 
 namespace sb {
 
@@ -109,7 +110,113 @@ myers_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ patte
     out[p] = score <= e ? score : -1;
 }
 
+// Dibit records (pack.cuh; the host-pack upload format): the 2-bit code of
+// column c sits in byte c & 3 of word c >> 4, at bits 2 * ((c >> 2) & 3); N
+// rows (optional) mark N columns, which match nothing. Pattern and text use the
+// same code, so the code itself indexes Peq.
+__device__ __forceinline__ int dibit_code(const uint32_t* row, int c) {
+    return static_cast<int>((__ldg(row + (c >> 4)) >> (8 * (c & 3) + 2 * ((c >> 2) & 3))) & 3u);
+}
+__device__ __forceinline__ bool n_bit(const uint32_t* nrow, int c) {
+    return nrow != nullptr && ((__ldg(nrow + (c >> 5)) >> (c & 31)) & 1u);
+}
+
+template <int W>
+__global__ void __launch_bounds__(128)
+myers_dibit_kernel(const uint8_t* __restrict__ text, const uint8_t* __restrict__ pattern,
+                   const uint8_t* __restrict__ ntext, const uint8_t* __restrict__ npattern,
+                   long long n, int m, int e, int32_t* __restrict__ out) {
+    const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const size_t dp = dibit_pitch(m), np = nplane_pitch(m);
+    const uint32_t* P = reinterpret_cast<const uint32_t*>(pattern + p * dp);
+    const uint32_t* T = reinterpret_cast<const uint32_t*>(text + p * dp);
+    const uint32_t* PN = npattern ? reinterpret_cast<const uint32_t*>(npattern + p * np) : nullptr;
+    const uint32_t* TN = ntext ? reinterpret_cast<const uint32_t*>(ntext + p * np) : nullptr;
+    uint64_t peq[4][W];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int w = 0; w < W; ++w) peq[c][w] = 0ull;
+    // one row word = 16 columns; the N row word covering them holds 32
+    const int nw16 = (m + 15) / 16;
+    for (int w16 = 0; w16 < nw16; ++w16) {
+        const uint32_t x = __ldg(P + w16);
+        const uint32_t nb = PN ? (__ldg(PN + (w16 >> 1)) >> (16 * (w16 & 1))) : 0u;
+        const int word = w16 >> 2;  // 64-bit Peq word of these columns
+        const int base = (w16 & 3) * 16;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int c = (x >> (8 * (k & 3) + 2 * (k >> 2))) & 3;  // column 16 w16 + k
+            const uint64_t bit = ((nb >> k) & 1u) || 16 * w16 + k >= m ? 0ull : 1ull << (base + k);
+#pragma unroll
+            for (int w = 0; w < W; ++w)
+                if (w == word) {
+                    peq[0][w] |= c == 0 ? bit : 0ull;
+                    peq[1][w] |= c == 1 ? bit : 0ull;
+                    peq[2][w] |= c == 2 ? bit : 0ull;
+                    peq[3][w] |= c == 3 ? bit : 0ull;
+                }
+        }
+    }
+    uint64_t pv[W], mv[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        pv[w] = ~0ull;
+        mv[w] = 0ull;
+    }
+    const int last = (m - 1) >> 6;
+    const uint64_t last_high = 1ull << ((m - 1) & 63);
+    int score = m;
+    for (int w16 = 0; w16 < nw16; ++w16) {
+        const uint32_t x = __ldg(T + w16);
+        const uint32_t nb = TN ? (__ldg(TN + (w16 >> 1)) >> (16 * (w16 & 1))) : 0u;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            if (16 * w16 + k >= m) break;
+            const int c = ((nb >> k) & 1u) ? -1 : static_cast<int>((x >> (8 * (k & 3) + 2 * (k >> 2))) & 3u);
+            int h = 1;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                if (w > last) break;
+                uint64_t eq = 0ull;
+                if (c == 0) eq = peq[0][w];
+                if (c == 1) eq = peq[1][w];
+                if (c == 2) eq = peq[2][w];
+                if (c == 3) eq = peq[3][w];
+                h = advance_block(pv[w], mv[w], eq, h, w == last ? last_high : (1ull << 63));
+            }
+            score += h;
+        }
+    }
+    out[p] = score <= e ? score : -1;
+}
+
 }  // namespace
+
+cudaError_t launch_edit_distance_dibits(const uint8_t* text, const uint8_t* pattern,
+                                        const uint8_t* ntext, const uint8_t* npattern, long long n,
+                                        int m, int e, int32_t* out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned grid = static_cast<unsigned>((n + 127) / 128);
+    const int words = (m + 63) / 64;
+#define SB_MD(W) myers_dibit_kernel<W><<<grid, 128, 0, s>>>(text, pattern, ntext, npattern, n, m, e, out)
+    if (words <= 1)
+        SB_MD(1);
+    else if (words <= 2)
+        SB_MD(2);
+    else if (words <= 4)
+        SB_MD(4);
+    else if (words <= 8)
+        SB_MD(8);
+    else if (words <= 16)
+        SB_MD(16);
+    else
+        return cudaErrorInvalidValue;
+#undef SB_MD
+    count_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_edit_distance(const uint8_t* text, const uint8_t* pattern, size_t pitch,
                                  long long n, int m, int e, int32_t* out, cudaStream_t s) {

@@ -99,6 +99,10 @@ cudaError_t launch_bits_transpose(const uint32_t* outplanes, long long n, int m,
 cudaError_t launch_repitch(const uint8_t* src, size_t src_stride, uint8_t* dst, size_t dst_pitch,
                            long long n, int m, cudaStream_t s);
 // Exact Levenshtein distance per pair (Myers bit-vector); out[i] = d <= e ? d : -1.
+// The same from dibit records (+ optional N rows), the host-pack upload format.
+cudaError_t launch_edit_distance_dibits(const uint8_t* text, const uint8_t* pattern,
+                                        const uint8_t* ntext, const uint8_t* npattern, long long n,
+                                        int m, int e, int32_t* out, cudaStream_t s);
 cudaError_t launch_edit_distance(const uint8_t* text, const uint8_t* pattern, size_t pitch,
                                  long long n, int m, int e, int32_t* out, cudaStream_t s);
 // MAGNET (magnet.cu): one thread per pair, validated ASCII records, 0 <= e < m,
