@@ -321,7 +321,8 @@ static FilterArgs resolve_nflags(const FilterArgs& args) {
 }
 
 static cudaError_t launch_pack_of(const FilterArgs& a, cudaStream_t s) {
-    return a.packed_text ? launch_pack_planes(a.packed_text, a.packed_pattern, a.n, a.m, a.planes, s)
+    return a.packed_text ? launch_pack_planes(a.packed_text, a.packed_pattern, a.n, a.m, a.planes, s,
+                                              a.nflags)
            : a.dibits    ? launch_pack_dibits(a.text, a.pattern, a.ntext, a.npattern, a.n, a.m,
                                               a.planes, s, a.nflags)
            : a.nibbles   ? launch_pack_nibbles(a.text, a.pattern, a.n, a.m, a.planes, s, a.nflags)
@@ -349,7 +350,8 @@ cudaError_t launch_filter(const FilterArgs& args, cudaStream_t s) {
         return cudaErrorInvalidValue;
     FilterArgs a = resolve_nflags(args);
     cudaError_t st =
-        a.packed_text ? launch_pack_planes(a.packed_text, a.packed_pattern, a.n, a.m, a.planes, s)
+        a.packed_text ? launch_pack_planes(a.packed_text, a.packed_pattern, a.n, a.m, a.planes, s,
+                                           a.nflags)
         : a.dibits    ? launch_pack_dibits(a.text, a.pattern, a.ntext, a.npattern, a.n, a.m,
                                            a.planes, s, a.nflags)
         : a.nibbles   ? launch_pack_nibbles(a.text, a.pattern, a.n, a.m, a.planes, s, a.nflags)

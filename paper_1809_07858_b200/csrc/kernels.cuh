@@ -79,8 +79,12 @@ cudaError_t launch_pack_dibits(const uint8_t* text, const uint8_t* pattern, cons
                                cudaStream_t s,
                                uint32_t* nflags = nullptr);
 // Stage 1 from packed_sequence planes ([n][3][ceil(m/64)] u64 per sequence).
+// packed_sequence planes (16-byte aligned, ceil(m/64) <= 8) can also write the
+// N-presence flags (pack.cuh).
+bool pack_planes_writes_nflags(const uint64_t* text, const uint64_t* pattern, int m);
 cudaError_t launch_pack_planes(const uint64_t* text, const uint64_t* pattern, long long n, int m,
-                               uint32_t* planes, cudaStream_t s);
+                               uint32_t* planes, cudaStream_t s,
+                               uint32_t* nflags = nullptr);
 // Launch the filter (pack + width-4 search, or pack + generic). Returns a cudaError_t.
 cudaError_t launch_filter(const FilterArgs& a, cudaStream_t s);
 // One stage of launch_filter on its own stream: 1 = pack into a.planes, 2 = search

@@ -170,7 +170,7 @@ static bool tile_nflags_fit(size_t pitch, int m) {
 }
 
 bool pack_writes_nflags(const FilterArgs& a) {
-    if (a.packed_text) return false;
+    if (a.packed_text) return pack_planes_writes_nflags(a.packed_text, a.packed_pattern, a.m);
     if (a.dibits) return dibit_pack_fits(a.m);
     if (a.nibbles) return tile_nflags_fit(nibble_pitch(a.m), a.m);
     return a.pitch % 4 == 0 && tile_nflags_fit(a.pitch, a.m);

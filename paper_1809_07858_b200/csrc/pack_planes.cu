@@ -70,7 +70,8 @@ struct Transpose32 {
 template <int W64>
 __global__ void __launch_bounds__(256)
 pack_planes_kernel(const uint64_t* __restrict__ text, const uint64_t* __restrict__ pattern,
-                   long long n, int m, uint32_t* __restrict__ planes) {
+                   long long n, int m, uint32_t* __restrict__ planes,
+                   uint32_t* __restrict__ nflags) {
     constexpr int RW = 6 * W64;  // u32 words per pair row
     extern __shared__ __align__(128) uint32_t smem[];
     __shared__ __align__(8) uint64_t bar;
@@ -109,12 +110,28 @@ pack_planes_kernel(const uint64_t* __restrict__ text, const uint64_t* __restrict
 #pragma unroll
         for (int q = 0; q < RW; ++q) r[q] = 0u;
     }
+    // N-presence (nflags, pack.cuh): a group whose 32 rows hold no N stores no N
+    // planes — the search then drops its N terms — and a block without any N
+    // skips its N region altogether
+    __shared__ int block_n;
+    if (threadIdx.x == 0) block_n = 0;
+    uint32_t nz = 0u;
+#pragma unroll
+    for (int j = 0; j < 2 * W64; ++j) nz |= r[2 * 2 * W64 + j];
+    const bool group_n = nflags == nullptr || __any_sync(~0u, nz != 0u);
+    __syncthreads();  // block_n initialised
+    if (group_n && lane == 0) block_n = 1;
+    const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
+    const long long g0 = static_cast<long long>(blockIdx.x) * kPackGroups;
+    if (nflags != nullptr && lane == 0 && g0 + gw < (n + 31) / 32)
+        nflags[nflag_index(s, g0 + gw, nblocks)] = group_n ? 1u : 0u;
     const Transpose32 transpose32(lane);
 #pragma unroll
     for (int j = 0; j < 2 * W64; ++j) {
         if (32 * j < m) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
+                if (k == 2 && !group_n) break;  // warp-uniform
                 const uint32_t col_word = transpose32(r[k * 2 * W64 + j]);
                 const int col = 32 * j + lane;
                 if (col < m) out[col * kOut + k * kPackGroups + gw] = col_word;
@@ -122,8 +139,6 @@ pack_planes_kernel(const uint64_t* __restrict__ text, const uint64_t* __restrict
         }
     }
     __syncthreads();
-    const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
-    const long long g0 = static_cast<long long>(blockIdx.x) * kPackGroups;
     // lo/hi region: 16 words per column (image words 0..15), then the N region:
     // 8 words per column (image words 16..23)
     uint4* dst = reinterpret_cast<uint4*>(planes + lohi_index(s, g0, 0, 0, nblocks, plane_cols(m)));
@@ -131,6 +146,7 @@ pack_planes_kernel(const uint64_t* __restrict__ text, const uint64_t* __restrict
         const uint32_t* src_w = out + (c >> 2) * kOut + 4 * (c & 3);
         dst[c] = make_uint4(src_w[0], src_w[1], src_w[2], src_w[3]);
     }
+    if (!block_n) return;  // no group of this block reads its N planes
     uint4* ndst = reinterpret_cast<uint4*>(planes + nplane_index(s, g0, 0, nblocks, plane_cols(m)));
     for (int c = threadIdx.x; c < m * kNColWords / 4; c += blockDim.x) {
         const uint32_t* src_w = out + (c >> 1) * kOut + kLhColWords + 4 * (c & 1);
@@ -176,10 +192,22 @@ pack_planes_direct_kernel(const uint64_t* __restrict__ text, const uint64_t* __r
 
 }  // namespace
 
+bool pack_planes_writes_nflags(const uint64_t* text, const uint64_t* pattern, int m) {
+    const bool aligned =
+        (reinterpret_cast<uintptr_t>(text) | reinterpret_cast<uintptr_t>(pattern)) % 16 == 0;
+    return (m + 63) / 64 <= 8 && pack_planes_smem(m) <= 200 * 1024 && aligned;
+}
+
 cudaError_t launch_pack_planes(const uint64_t* text, const uint64_t* pattern, long long n, int m,
-                               uint32_t* planes, cudaStream_t s) {
+                               uint32_t* planes, cudaStream_t s, uint32_t* nflags) {
     if (n <= 0) return cudaSuccess;
     if (planes == nullptr || m <= 0) return cudaErrorInvalidValue;
+    if (nflags && !pack_planes_writes_nflags(text, pattern, m)) return cudaErrorInvalidValue;
+    if (nflags) {  // the all-zero N column image N-free groups of mixed warps read
+        const cudaError_t st = cudaMemsetAsync(nflags + nflag_words(n), 0,
+                                               nzero_words(m) * sizeof(uint32_t), s);
+        if (st != cudaSuccess) return st;
+    }
     const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
     const dim3 grid(static_cast<unsigned>(nblocks), 2);
     const size_t smem = pack_planes_smem(m);
@@ -192,7 +220,7 @@ cudaError_t launch_pack_planes(const uint64_t* text, const uint64_t* pattern, lo
     case W: {                                                                                  \
         const cudaError_t st = ensure_smem_attr<pack_planes_kernel<W>>(200 * 1024);            \
         if (st != cudaSuccess) return st;                                                      \
-        pack_planes_kernel<W><<<grid, 32 * kPackGroups, smem, s>>>(text, pattern, n, m, planes); \
+        pack_planes_kernel<W><<<grid, 32 * kPackGroups, smem, s>>>(text, pattern, n, m, planes, nflags); \
         break;                                                                                 \
     }
             SB_PP(1) SB_PP(2) SB_PP(3) SB_PP(4) SB_PP(5) SB_PP(6) SB_PP(7) SB_PP(8)

@@ -103,3 +103,17 @@ def test_device_entry_point(gpu, oracle):
     assert (acc.cpu().numpy().view(np.uint32) == a2).all()
     assert (est.cpu().numpy().view(np.uint32) == e2).all()
     assert (bits.cpu().numpy().view(np.uint64) == b2).all()
+
+
+def test_mixed_n_presence(gpu, oracle):
+    """N-presence flags of the re-slice: most groups N-free (N planes neither stored nor read),
+    a few holding an N in the text or the pattern (warps mixing both kinds), and blocks with
+    no N at all (their N region is skipped)."""
+    rng = np.random.default_rng(77)
+    n, m = 40_000, 100
+    t, p = pairs(rng, n, m, alphabet=ACGT)
+    for i in rng.choice(n, size=300, replace=False):
+        (t if rng.random() < 0.5 else p)[i, int(rng.integers(0, m))] = ord("N")
+    for e in (0, 2, 5, 10, 13):
+        check(gpu, oracle, t, p, e, bits=False)
+    check(gpu, oracle, t[:5000], p[:5000], 5, bits=True)
