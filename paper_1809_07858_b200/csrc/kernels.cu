@@ -308,7 +308,9 @@ static bool nflags_enabled() {
     return v;
 }
 
-static bool search_reads_nflags(const FilterArgs& a) { return use_fused(a.width, a.e, a.m); }
+static bool search_reads_nflags(const FilterArgs& a) {
+    return use_fused(a.width, a.e, a.m) || (wsearch_enabled() && wsearch_applies(a));
+}
 
 // The N-presence flag region both stages agree on (or null).
 static FilterArgs resolve_nflags(const FilterArgs& args) {

@@ -13,7 +13,7 @@ cudaError_t launch_w(const FilterArgs& a, cudaStream_t s) {
     const long long ngroups = (a.n + 31) / 32;
     const unsigned grid = static_cast<unsigned>((ngroups + 127) / 128);
     shouji_wsearch<W, NC><<<grid, 128, 0, s>>>(a.planes, a.n, a.m, static_cast<int>(a.e), a.accept,
-                                               a.estimates, a.outplanes);
+                                               a.estimates, a.outplanes, a.nflags);
     count_launch();
     return cudaGetLastError();
 }

@@ -95,7 +95,9 @@ struct CandW {
     uint32_t s[W - 1];           // slice bits 1 .. W-1
 };
 
-template <int W, bool CHECK>
+// NOPN: the warp's groups are N-free (N-presence flags): no N loads, and a
+// 2-LOP3 map word in interior blocks (fused.cuh, load_rel / map_word).
+template <int W, bool CHECK, bool NOPN = false>
 __device__ __forceinline__ void wsearch_block(const uint32_t* __restrict__ tbase,
                                               const uint32_t* __restrict__ tnbase, int tcol0,
                                               const uint32_t* __restrict__ pbase,
@@ -107,16 +109,15 @@ __device__ __forceinline__ void wsearch_block(const uint32_t* __restrict__ tbase
     constexpr int NO = WPlanes<W>::NO;
     uint32_t T[X][3];
 #pragma unroll
-    for (int x = 0; x < X; ++x) load_rel<CHECK, true>(tbase, tnbase, x, tcol0, m, T[x]);
+    for (int x = 0; x < X; ++x) load_rel<CHECK, true, NOPN>(tbase, tnbase, x, tcol0, m, T[x]);
     uint32_t P[X][3];
 #pragma unroll
-    for (int x = 0; x < X; ++x) load_rel<CHECK, true>(pbase, pnbase, x, pcol0, m, P[x]);
+    for (int x = 0; x < X; ++x) load_rel<CHECK, true, NOPN>(pbase, pnbase, x, pcol0, m, P[x]);
     auto step = [&](const int rot, bool first) {
         uint32_t sv[X];
 #pragma unroll
         for (int x = 0; x < X; ++x) {
-            const uint32_t* pp = P[(rot + x) % X];
-            sv[x] = (pp[0] ^ T[x][0]) | (pp[1] ^ T[x][1]) | pp[2] | T[x][2];
+            sv[x] = map_word<NOPN && !CHECK>(P[(rot + x) % X], T[x]);
         }
 #pragma unroll
         for (int b = 0; b < B; ++b) {
@@ -148,7 +149,7 @@ __device__ __forceinline__ void wsearch_block(const uint32_t* __restrict__ tbase
         for (int u = 0; u < X; ++u) {
             const int di = d0 + u;
             if (di > 2 * E) break;
-            load_rel<CHECK, true>(pbase, pnbase, di + X - 1, pcol0, m, P[u]);
+            load_rel<CHECK, true, NOPN>(pbase, pnbase, di + X - 1, pcol0, m, P[u]);
             step((1 + u) % X, false);
         }
     }
@@ -173,12 +174,15 @@ __device__ __forceinline__ uint32_t fsm_step_w(const CandW<W>& best, uint32_t (&
 }
 
 // The whole sweep for group g (32 pairs): NB blocks of 4 windows.
-template <int W, int NC>
+// NOPN / zero / tzero / pzero: as search_group (fused.cuh).
+template <int W, int NC, bool NOPN = false>
 __device__ __forceinline__ void wsearch_group(const uint32_t* __restrict__ planes, long long g,
                                               long long n, int m, int E,
                                               uint32_t* __restrict__ accept,
                                               uint32_t* __restrict__ estimates,
-                                              uint32_t* __restrict__ outplanes) {
+                                              uint32_t* __restrict__ outplanes,
+                                              const uint32_t* __restrict__ zero = nullptr,
+                                              bool tzero = false, bool pzero = false) {
     constexpr int B = 4;
     constexpr int X = B + W - 1;
     const long long row0 = g * 32;
@@ -188,8 +192,8 @@ __device__ __forceinline__ void wsearch_group(const uint32_t* __restrict__ plane
     const int mc = plane_cols(m);
     const uint32_t* const tb = planes + lohi_index(0, g, 0, 0, nblocks, mc);
     const uint32_t* const pb = planes + lohi_index(1, g, 0, 0, nblocks, mc);
-    const uint32_t* const tnb = planes + nplane_index(0, g, 0, nblocks, mc);
-    const uint32_t* const pnb = planes + nplane_index(1, g, 0, nblocks, mc);
+    const uint32_t* const tnb = tzero ? zero + g % kPackGroups : planes + nplane_index(0, g, 0, nblocks, mc);
+    const uint32_t* const pnb = pzero ? zero + g % kPackGroups : planes + nplane_index(1, g, 0, nblocks, mc);
     uint32_t S[W - 1];
 #pragma unroll
     for (int i = 0; i < W - 1; ++i) S[i] = ~0u;  // bitvector bv(m, true) (shouji.cpp:52)
@@ -208,9 +212,9 @@ __device__ __forceinline__ void wsearch_group(const uint32_t* __restrict__ plane
         const uint32_t* pnbase = pnb + static_cast<long long>(pcol0) * kNColWords;
         CandW<W> best[B];
         if (interior)
-            wsearch_block<W, false>(tbase, tnbase, j0, pbase, pnbase, pcol0, m, E, best);
+            wsearch_block<W, false, NOPN>(tbase, tnbase, j0, pbase, pnbase, pcol0, m, E, best);
         else
-            wsearch_block<W, true>(tbase, tnbase, j0, pbase, pnbase, pcol0, m, E, best);
+            wsearch_block<W, true, NOPN>(tbase, tnbase, j0, pbase, pnbase, pcol0, m, E, best);
         uint32_t outs[B];
 #pragma unroll
         for (int b = 0; b < B; ++b) {
@@ -243,8 +247,21 @@ template <int W, int NC>
 __global__ void __launch_bounds__(128)
 shouji_wsearch(const uint32_t* __restrict__ planes, long long n, int m, int E,
                uint32_t* __restrict__ accept, uint32_t* __restrict__ estimates,
-               uint32_t* __restrict__ outplanes) {
+               uint32_t* __restrict__ outplanes, const uint32_t* __restrict__ nflags) {
     const long long g = static_cast<long long>(blockIdx.x) * 128 + threadIdx.x;
+    if (nflags != nullptr) {  // as shouji_search_w4 (fused.cuh)
+        const long long nblocks = (n + kPackPairs - 1) / kPackPairs;
+        const bool live = g * 32 < n;
+        const bool tz = !live || nflags[nflag_index(0, g, nblocks)] == 0u;
+        const bool pz = !live || nflags[nflag_index(1, g, nblocks)] == 0u;
+        if (__all_sync(~0u, tz && pz)) {
+            wsearch_group<W, NC, true>(planes, g, n, m, E, accept, estimates, outplanes);
+            return;
+        }
+        wsearch_group<W, NC, false>(planes, g, n, m, E, accept, estimates, outplanes,
+                                    nflags + nflag_words(n), tz, pz);
+        return;
+    }
     wsearch_group<W, NC>(planes, g, n, m, E, accept, estimates, outplanes);
 }
 
