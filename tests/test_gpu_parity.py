@@ -208,6 +208,25 @@ def test_generic_widths(gpu, oracle, width):
         check_batch(gpu, oracle, t, p, e, width, bits=True)
 
 
+@pytest.mark.parametrize("width", [3, 5, 8])
+def test_generic_widths_mixed_n_presence(gpu, oracle, width):
+    """The any-width search's N-presence paths: warps of N-free groups (no N terms), warps
+    mixing N-free groups (reading the zero image) with groups holding an N, and width 4 with
+    E > 31 on the same kernel."""
+    rng = np.random.default_rng(100 + width)
+    n, m = 20_000, 100
+    t = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=(n, m))]
+    p = t.copy()
+    mask = rng.random(p.shape) < 0.05
+    p[mask] = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, size=int(mask.sum()))]
+    for i in rng.choice(n, size=150, replace=False):
+        (t if rng.random() < 0.5 else p)[i, int(rng.integers(0, m))] = ord("N")
+    for e in (2, 5, 12):
+        check_batch(gpu, oracle, t, p, e, width)
+    if width == 3:
+        check_batch(gpu, oracle, t[:3000], p[:3000], 35, 4)
+
+
 def test_large_threshold_generic_path(gpu, oracle):
     rng = np.random.default_rng(5)
     for m, e in [(200, 150), (100, 32), (250, 60), (300, 20), (600, 10)]:
